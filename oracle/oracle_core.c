@@ -1,0 +1,409 @@
+/*
+ * oracle_core.c -- plain scalar C core of the CPU ORACLE.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * legs load this library.  It shares no code, header or table with the product
+ * library (paper_2511_00737_b200/csrc); it is compiled by gcc, not nvcc.
+ *
+ * Everything follows the plain definitions:
+ *   - modular product: (unsigned __int128)a*b % q                      (no Barrett/Shoup)
+ *   - negacyclic NTT : the textbook Cooley-Tukey / Gentleman-Sande loops over
+ *                      Z_q[X]/(X^N+1) (the BFV ring of PAPER.md l.135), output
+ *                      index i = evaluation at psi^(2*brev(i)+1) (DESIGN.md
+ *                      reading #1); pinned in tests against O(N^2) direct
+ *                      evaluation and schoolbook negacyclic products.
+ *   - slot encode    : inverse NTT mod t ("packing"; reading #1)
+ *   - encryption     : symmetric BFV, c1 = a, c0 = NTT(Delta*m + e) - a*s
+ *                      ("encrypted ... using a given secret key"; readings #4-#6)
+ *   - client eval    : acc_j = sum_d c_{d,j} (.) NTT_j(lift_j(encode(v_{b,d})))
+ *                      (D MulCP, D-1 AddCC, 0 Rot)
+ *   - randomness     : SplitMix64 streams of DESIGN.md reading #7-#11.
+ * OpenMP only splits independent dims d across threads; each thread runs the
+ * same plain loop and the per-thread sums are added mod q at the end.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+typedef unsigned __int128 u128;
+
+/* ------------------------------------------------------------------ */
+/* plain modular arithmetic                                            */
+/* ------------------------------------------------------------------ */
+u64 or_mulmod(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+u64 or_addmod(u64 a, u64 b, u64 q) { return (u64)(((u128)a + b) % q); }
+u64 or_submod(u64 a, u64 b, u64 q) { return (u64)(((u128)a + q - b) % q); }
+
+u64 or_powmod(u64 a, u64 e, u64 q) {
+    u64 r = 1 % q;
+    a %= q;
+    while (e) {
+        if (e & 1) r = or_mulmod(r, a, q);
+        a = or_mulmod(a, a, q);
+        e >>= 1;
+    }
+    return r;
+}
+
+u32 or_brev(u32 i, int bits) {
+    u32 r = 0;
+    for (int b = 0; b < bits; ++b) { r = (r << 1) | (i & 1); i >>= 1; }
+    return r;
+}
+
+/* table[i] = x^brev(i) mod q, i < N (x = psi for forward, psi^-1 for inverse) */
+void or_pow_brev_table(u64 x, u64 q, int logN, u64 *table) {
+    u32 N = 1u << logN;
+    for (u32 i = 0; i < N; ++i) table[i] = or_powmod(x, or_brev(i, logN), q);
+}
+
+/* ------------------------------------------------------------------ */
+/* textbook negacyclic NTT                                             */
+/* ------------------------------------------------------------------ */
+/* forward: natural-order coefficients -> a[i] = A(psi^(2 brev(i) + 1)) */
+void or_ntt_fwd(u64 *a, int logN, u64 q, const u64 *psi_rev) {
+    u32 N = 1u << logN;
+    u32 t = N;
+    for (u32 m = 1; m < N; m <<= 1) {
+        t >>= 1;
+        for (u32 i = 0; i < m; ++i) {
+            u64 w = psi_rev[m + i];
+            u32 j1 = 2 * i * t;
+            for (u32 j = j1; j < j1 + t; ++j) {
+                u64 U = a[j];
+                u64 V = or_mulmod(a[j + t], w, q);
+                a[j] = or_addmod(U, V, q);
+                a[j + t] = or_submod(U, V, q);
+            }
+        }
+    }
+}
+
+/* inverse of or_ntt_fwd (Gentleman-Sande with psi^-1, then times N^-1) */
+void or_ntt_inv(u64 *a, int logN, u64 q, const u64 *psiinv_rev) {
+    u32 N = 1u << logN;
+    u32 t = 1;
+    for (u32 m = N; m > 1; m >>= 1) {
+        u32 h = m >> 1;
+        u32 j1 = 0;
+        for (u32 i = 0; i < h; ++i) {
+            u64 w = psiinv_rev[h + i];
+            for (u32 j = j1; j < j1 + t; ++j) {
+                u64 U = a[j];
+                u64 V = a[j + t];
+                a[j] = or_addmod(U, V, q);
+                a[j + t] = or_mulmod(or_submod(U, V, q), w, q);
+            }
+            j1 += 2 * t;
+        }
+        t <<= 1;
+    }
+    u64 ninv = or_powmod(N, q - 2, q);
+    for (u32 j = 0; j < N; ++j) a[j] = or_mulmod(a[j], ninv, q);
+}
+
+/* batched wrappers: polys[n][N] all mod q */
+void or_ntt_fwd_many(u64 *polys, u64 n, int logN, u64 q, u64 psi) {
+    u32 N = 1u << logN;
+    u64 *tab = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(psi, q, logN, tab);
+    #pragma omp parallel for schedule(static)
+    for (long long p = 0; p < (long long)n; ++p) or_ntt_fwd(polys + (u64)p * N, logN, q, tab);
+    free(tab);
+}
+
+void or_ntt_inv_many(u64 *polys, u64 n, int logN, u64 q, u64 psi) {
+    u32 N = 1u << logN;
+    u64 *tab = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(or_powmod(psi, q - 2, q), q, logN, tab);
+    #pragma omp parallel for schedule(static)
+    for (long long p = 0; p < (long long)n; ++p) or_ntt_inv(polys + (u64)p * N, logN, q, tab);
+    free(tab);
+}
+
+/* Horner evaluation a(x) mod q: the definition of an NTT output point */
+u64 or_eval(const u64 *a, u32 N, u64 q, u64 x) {
+    u64 r = 0;
+    for (u32 n = N; n-- > 0;) r = or_addmod(or_mulmod(r, x, q), a[n], q);
+    return r;
+}
+
+/* schoolbook product in Z_q[X]/(X^N + 1) */
+void or_negacyclic_mul(const u64 *a, const u64 *b, u64 *c, u32 N, u64 q) {
+    for (u32 i = 0; i < N; ++i) c[i] = 0;
+    for (u32 i = 0; i < N; ++i)
+        for (u32 j = 0; j < N; ++j) {
+            u64 p = or_mulmod(a[i], b[j], q);
+            u32 k = i + j;
+            if (k < N) c[k] = or_addmod(c[k], p, q);
+            else c[k - N] = or_submod(c[k - N], p, q);
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* randomness: SplitMix64 streams (reading #7)               */
+/* ------------------------------------------------------------------ */
+#define GOLD 0x9E3779B97F4A7C15ULL
+u64 or_mix64(u64 z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+u64 or_stream(u64 seed, u64 tag, u64 a, u64 b) {
+    u64 h = or_mix64(seed ^ (tag * GOLD));
+    h = or_mix64(h ^ (a * 0xD1B54A32D192ED03ULL));
+    return or_mix64(h ^ (b * 0x8CB92BA72F3D8DD7ULL));
+}
+/* n-th output of SplitMix64 whose state starts at st */
+u64 or_draw(u64 st, u64 n) { return or_mix64(st + (n + 1) * GOLD); }
+
+enum { TAG_SK = 2, TAG_A = 3, TAG_E = 4, TAG_RES = 6 };
+
+/* reading #9: s_i = (next() mod 3) - 1 */
+void or_sample_ternary(u64 seed, u32 N, int8_t *s) {
+    for (u32 i = 0; i < N; ++i) s[i] = (int8_t)((int)(or_draw(or_stream(seed, TAG_SK, 0, i), 0) % 3) - 1);
+}
+
+static u64 bitmask_for(u64 q) {
+    u64 m = 1;
+    while (m < q) m = (m << 1) | 1;   /* 2^ceil(log2 q) - 1 (q is never a power of two) */
+    return m;
+}
+/* reading #8: uniform mod q by rejection; stream index (d*L + j, i) */
+u64 or_uniform_mod(u64 seed, u64 d, u32 j, u32 L, u32 i, u64 q) {
+    u64 st = or_stream(seed, TAG_A, d * L + j, i);
+    u64 mask = bitmask_for(q);
+    for (u64 n = 0;; ++n) {
+        u64 u = or_draw(st, n) & mask;
+        if (u < q) return u;
+    }
+}
+/* reading #10: CDT over magnitudes, sign from a second draw */
+long long or_gauss(u64 seed, u64 d, u32 i, const u64 *cdt, int ncdt) {
+    u64 st = or_stream(seed, TAG_E, d, i);
+    u64 u = or_draw(st, 0) >> 1;
+    int k = 0;
+    while (k < ncdt - 1 && u >= cdt[k]) ++k;
+    if (k == 0) return 0;
+    return (or_draw(st, 1) >> 63) ? -(long long)k : (long long)k;
+}
+
+void or_sample_uniform_poly(u64 seed, u64 d, u32 j, u32 L, u64 q, u32 N, u64 *out) {
+    for (u32 i = 0; i < N; ++i) out[i] = or_uniform_mod(seed, d, j, L, i, q);
+}
+void or_sample_gauss_poly(u64 seed, u64 d, u32 N, const u64 *cdt, int ncdt, long long *e) {
+    for (u32 i = 0; i < N; ++i) e[i] = or_gauss(seed, d, i, cdt, ncdt);
+}
+
+/* ------------------------------------------------------------------ */
+/* BFV pieces of the method                                            */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int logN;
+    u32 L;
+    const u64 *q;        /* [L] */
+    const u64 *psi;      /* [L] */
+    u64 t;
+    u64 psi_t;
+    u32 k;
+    u32 D_live;
+    const u64 *delta;    /* [L]  floor(Q/t) mod q_j */
+    const u64 *s_hat;    /* [L][N] NTT_j(s) */
+    u64 enc_seed;
+    const u64 *cdt;
+    int ncdt;
+} or_bfv;
+
+static u64 lift_centered(u64 m, u64 t, u64 q) {
+    /* reading #3: m in [0,t) -> m if m <= (t-1)/2 else m - t + q (mod q) */
+    if (m <= (t - 1) / 2) return m % q;
+    return or_submod(m % q, t % q, q);
+}
+
+/* model tile of dim d: slot i <- C[i mod k][d] for i < k*floor(N/k), else 0
+   (P:650-653 / P:1471-1474: k-fold interleave, B = floor(N/k)); returns m_d */
+static void model_plaintext(const or_bfv *P, const int8_t *class_hv, u32 d, const u64 *tinv_tab, u64 *m) {
+    u32 N = 1u << P->logN;
+    u32 B = N / P->k;
+    for (u32 i = 0; i < N; ++i) {
+        long long v = (i < P->k * B) ? class_hv[(u64)(i % P->k) * P->D_live + d] : 0;
+        m[i] = (u64)((v % (long long)P->t + (long long)P->t) % (long long)P->t);
+    }
+    or_ntt_inv(m, P->logN, P->t, tinv_tab);
+}
+
+/* ciphertext of dim d, all primes: out[L][2][N] canonical NTT form */
+static void encrypt_dim(const or_bfv *P, const int8_t *class_hv, u32 d, const u64 *tinv_tab,
+                        u64 *const *psi_tabs, u64 *m, long long *e, u64 *x, u64 *out) {
+    u32 N = 1u << P->logN;
+    model_plaintext(P, class_hv, d, tinv_tab, m);
+    or_sample_gauss_poly(P->enc_seed, d, N, P->cdt, P->ncdt, e);
+    for (u32 j = 0; j < P->L; ++j) {
+        u64 q = P->q[j];
+        for (u32 i = 0; i < N; ++i) {
+            u64 ei = e[i] >= 0 ? (u64)e[i] % q : or_submod(0, (u64)(-e[i]) % q, q);
+            x[i] = or_addmod(or_mulmod(P->delta[j], m[i] % q, q), ei, q);   /* Delta*m + e, m in [0,t) */
+        }
+        or_ntt_fwd(x, P->logN, q, psi_tabs[j]);
+        u64 *c0 = out + ((u64)j * 2 + 0) * N;
+        u64 *c1 = out + ((u64)j * 2 + 1) * N;
+        for (u32 i = 0; i < N; ++i) {
+            u64 a = or_uniform_mod(P->enc_seed, d, j, P->L, i, q);
+            c1[i] = a;
+            c0[i] = or_submod(x[i], or_mulmod(a, P->s_hat[(u64)j * N + i], q), q);
+        }
+    }
+}
+
+static u64 **make_psi_tabs(const or_bfv *P, int inverse) {
+    u32 N = 1u << P->logN;
+    u64 **tabs = (u64 **)malloc(sizeof(u64 *) * P->L);
+    for (u32 j = 0; j < P->L; ++j) {
+        tabs[j] = (u64 *)malloc(sizeof(u64) * N);
+        u64 x = inverse ? or_powmod(P->psi[j], P->q[j] - 2, P->q[j]) : P->psi[j];
+        or_pow_brev_table(x, P->q[j], P->logN, tabs[j]);
+    }
+    return tabs;
+}
+static void free_tabs(u64 **tabs, u32 L) { for (u32 j = 0; j < L; ++j) free(tabs[j]); free(tabs); }
+
+/* model ciphertexts for dims [d0, d0+nd): out[nd][L][2][N] */
+void or_encrypt_dims(const or_bfv *P, const int8_t *class_hv, u32 d0, u32 nd, u64 *out) {
+    u32 N = 1u << P->logN;
+    u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(or_powmod(P->psi_t, P->t - 2, P->t), P->t, P->logN, tinv);
+    u64 **fw = make_psi_tabs(P, 0);
+    #pragma omp parallel
+    {
+        u64 *m = (u64 *)malloc(sizeof(u64) * N);
+        u64 *x = (u64 *)malloc(sizeof(u64) * N);
+        long long *e = (long long *)malloc(sizeof(long long) * N);
+        #pragma omp for schedule(dynamic)
+        for (long long dd = 0; dd < (long long)nd; ++dd)
+            encrypt_dim(P, class_hv, d0 + (u32)dd, tinv, fw, m, e, x,
+                        out + (u64)dd * P->L * 2 * N);
+        free(m); free(x); free(e);
+    }
+    free(tinv);
+    free_tabs(fw, P->L);
+}
+
+/* query slot vector of (batch b, dim d): slot i <- h[d][b*B + i/k] for i < k*n_b, else 0 */
+static void query_plaintext(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d, const u64 *tinv, u64 *m) {
+    u32 N = 1u << P->logN;
+    u32 B = N / P->k;
+    u32 nb = nq - b * B < B ? nq - b * B : B;
+    for (u32 i = 0; i < N; ++i) {
+        long long v = (i < P->k * nb) ? H[(u64)d * nq + (u64)b * B + i / P->k] : 0;
+        m[i] = (u64)((v % (long long)P->t + (long long)P->t) % (long long)P->t);
+    }
+    or_ntt_inv(m, P->logN, P->t, tinv);      /* encode = INTT_t */
+}
+
+/* plaintext NTTs p_hat[b,d,j] for dims [d0,d0+nd): out[nd][L][N] */
+void or_plaintext_ntts(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0, u32 nd, u64 *out) {
+    u32 N = 1u << P->logN;
+    u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(or_powmod(P->psi_t, P->t - 2, P->t), P->t, P->logN, tinv);
+    u64 **fw = make_psi_tabs(P, 0);
+    #pragma omp parallel
+    {
+        u64 *m = (u64 *)malloc(sizeof(u64) * N);
+        #pragma omp for schedule(dynamic)
+        for (long long dd = 0; dd < (long long)nd; ++dd) {
+            query_plaintext(P, H, nq, b, d0 + (u32)dd, tinv, m);
+            for (u32 j = 0; j < P->L; ++j) {
+                u64 *p = out + ((u64)dd * P->L + j) * N;
+                for (u32 i = 0; i < N; ++i) p[i] = lift_centered(m[i], P->t, P->q[j]);
+                or_ntt_fwd(p, P->logN, P->q[j], fw[j]);
+            }
+        }
+        free(m);
+    }
+    free(tinv);
+    free_tabs(fw, P->L);
+}
+
+/* Client evaluation of batch b over dims [0, D_live):
+   one MulCP per dim (ct_d (x) pt_{b,d}), D-1 AddCC, no rotation:
+   acc[c][j][i] = sum_d ct_{d,j,c}[i] * p_hat_{b,d,j}[i]  (mod q_j), output [2][L][N].
+   model == NULL: each dim's ciphertext is re-encrypted on the fly from class_hv
+   (c4's model does not fit in host RAM); otherwise model is [D_live][L][2][N].
+   counters (may be NULL): [0] MulCP, [1] AddCC, [2] rotations. */
+void or_infer_batch(const or_bfv *P, const int8_t *H, u32 nq, u32 b,
+                    const u64 *model, const int8_t *class_hv, u64 *acc, u64 *counters) {
+    u32 N = 1u << P->logN;
+    u32 L = P->L;
+    u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(or_powmod(P->psi_t, P->t - 2, P->t), P->t, P->logN, tinv);
+    u64 **fw = make_psi_tabs(P, 0);
+    u64 n_mul = 0, n_add = 0;
+    int first_global = 1;
+    for (u64 x = 0; x < (u64)2 * L * N; ++x) acc[x] = 0;
+    #pragma omp parallel reduction(+ : n_mul, n_add)
+    {
+        u64 *m = (u64 *)malloc(sizeof(u64) * N);
+        u64 *p = (u64 *)malloc(sizeof(u64) * N);
+        u64 *ct = (u64 *)malloc(sizeof(u64) * L * 2 * N);
+        u64 *x = (u64 *)malloc(sizeof(u64) * N);
+        long long *e = (long long *)malloc(sizeof(long long) * N);
+        u64 *part = (u64 *)calloc((size_t)2 * L * N, sizeof(u64));
+        int have = 0;
+        #pragma omp for schedule(dynamic, 4)
+        for (long long dd = 0; dd < (long long)P->D_live; ++dd) {
+            u32 d = (u32)dd;
+            const u64 *c;
+            if (model) c = model + (u64)d * L * 2 * N;
+            else { encrypt_dim(P, class_hv, d, tinv, fw, m, e, x, ct); c = ct; }
+            query_plaintext(P, H, nq, b, d, tinv, m);
+            for (u32 j = 0; j < L; ++j) {
+                u64 q = P->q[j];
+                for (u32 i = 0; i < N; ++i) p[i] = lift_centered(m[i], P->t, q);
+                or_ntt_fwd(p, P->logN, q, fw[j]);
+                for (u32 cc = 0; cc < 2; ++cc) {
+                    const u64 *cj = c + ((u64)j * 2 + cc) * N;
+                    u64 *aj = part + ((u64)cc * L + j) * N;
+                    for (u32 i = 0; i < N; ++i) aj[i] = or_addmod(aj[i], or_mulmod(cj[i], p[i], q), q);
+                }
+            }
+            n_mul += 1;                 /* one ct x pt product (all primes, c0 and c1) */
+            if (have) n_add += 1;       /* folding a product into a running sum */
+            have = 1;
+        }
+        #pragma omp critical
+        {
+            if (have) {
+                if (!first_global) n_add += 1;   /* merging two partial sums is one more AddCC */
+                first_global = 0;
+                for (u32 cc = 0; cc < 2; ++cc)
+                    for (u32 j = 0; j < L; ++j)
+                        for (u32 i = 0; i < N; ++i) {
+                            u64 *a = acc + ((u64)cc * L + j) * N + i;
+                            *a = or_addmod(*a, part[((u64)cc * L + j) * N + i], P->q[j]);
+                        }
+            }
+        }
+        free(m); free(p); free(ct); free(x); free(e); free(part);
+    }
+    if (counters) { counters[0] = n_mul; counters[1] = n_add; counters[2] = 0; }
+    free(tinv);
+    free_tabs(fw, L);
+}
+
+/* decryption helper (per prime, NTT domain): x_hat = c0 + c1 (.) s_hat, then INTT_j.
+   ct: [2][L][N]; out: [L][N] coefficient form of the phase mod q_j */
+void or_decrypt_phase(const or_bfv *P, const u64 *ct, u64 *out) {
+    u32 N = 1u << P->logN;
+    u64 **inv = make_psi_tabs(P, 1);
+    for (u32 j = 0; j < P->L; ++j) {
+        u64 q = P->q[j];
+        const u64 *c0 = ct + ((u64)0 * P->L + j) * N;
+        const u64 *c1 = ct + ((u64)1 * P->L + j) * N;
+        u64 *o = out + (u64)j * N;
+        for (u32 i = 0; i < N; ++i) o[i] = or_addmod(c0[i], or_mulmod(c1[i], P->s_hat[(u64)j * N + i], q), q);
+        or_ntt_inv(o, P->logN, q, inv[j]);
+    }
+    free_tabs(inv, P->L);
+}
