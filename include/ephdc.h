@@ -1,0 +1,234 @@
+/*
+ * ephdc.h -- C ABI of libephdc.so, the B200 (sm_100a) hot path of EP-HDC's
+ * client-side encrypted HDC inference (arXiv 2511.00737).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n
+ * (both only on the build box), readings "#n" = DESIGN.md section "Readings".
+ *
+ * The problem: the server holds the secret key and encrypts the k
+ * class hypervectors ONCE as D ciphertexts (slot i of ciphertext d holds
+ * C[i mod k][d], P:650-653 / P:1471-1474); the client packs B = floor(N/k)
+ * plaintext query hypervectors into D plaintexts (slot i of plaintext d holds
+ * h[d][query i/k]) and evaluates sum_d CT_d (x) PT_d -- D ct*pt multiplies,
+ * D-1 ct+ct adds, 0 rotations -- returning one scores
+ * ciphertext per batch of B queries, which the server decrypts.
+ *
+ * Conventions (all entry points):
+ *  - Return an ephdc_status; no exception crosses the ABI, nothing aborts.
+ *  - Opaque handles (ctx, sk, model, workspace, ntt_plan) are owned by the
+ *    library: create/free pairs; *_free(NULL) is a no-op.  Handles are
+ *    immutable after creation except the workspace, which one stream at a
+ *    time may use.
+ *  - "d_" pointers are DEVICE pointers on the context's device, "h_" pointers
+ *    are HOST pointers; both are caller-owned and only borrowed for the call.
+ *  - Device work is enqueued asynchronously on `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream); a launch failure returns
+ *    EPHDC_ECUDA immediately.  Calls documented as "synchronous" finish all
+ *    their device work before returning.
+ *  - Layouts are C row-major, little-endian; residues are canonical in [0, p)
+ *    at every boundary (reading #24).
+ *  - Decryption failure (noise overflow) is NOT an error.
+ *  - No CPU fallback: every compute entry point runs CUDA kernels; if no
+ *    device is usable it returns EPHDC_ECUDA.
+ */
+#ifndef EPHDC_H
+#define EPHDC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EPHDC_ABI_VERSION 1
+#define EPHDC_MAX_PRIMES 16
+
+typedef enum {
+    EPHDC_OK = 0,
+    EPHDC_EPARAM = 1,     /* bad N, t, q, sizes                      */
+    EPHDC_ECONTEXT = 2,   /* handle from another context / host-only context       */
+    EPHDC_EOVERFLOW = 3,  /* output capacity < ceil(nq / B) ciphertexts     */
+    EPHDC_ERESOURCE = 4,  /* allocation failed                                     */
+    EPHDC_ECUDA = 5,      /* CUDA error (no device, launch or copy failure)        */
+    EPHDC_EDOMAIN = 6,    /* value outside its modular domain                      */
+    EPHDC_ENULL = 7       /* required pointer is NULL                              */
+} ephdc_status;
+
+/* BFV + HDC parameter set (S8 of SURVEY.md; BASELINE.json configs). */
+typedef struct {
+    uint32_t log2N;          /* ring degree N = 2^log2N, 10 <= log2N <= 14        */
+    uint32_t L;              /* number of RNS primes, 1..EPHDC_MAX_PRIMES         */
+    const uint64_t *q;       /* [L] distinct primes = 1 mod 2N, < 2^60, != t      */
+    uint64_t t;              /* plaintext modulus: prime = 1 mod 2N, < 2^30       */
+    uint32_t k;              /* classes, 1 <= k <= N                              */
+    uint32_t D_live;         /* hypervector dimension used by the model           */
+    uint32_t D_stored;       /* rows of the projection base (>= D_live; padding)  */
+    uint32_t F;              /* features per query, multiple of 4                 */
+    uint32_t feat_unsigned;  /* 0: int8 features, 1: uint8 features               */
+    uint32_t Qbits;          /* query HV width, 2..8 (reading #12)  */
+    uint32_t Cbits;          /* class HV width, 2..8                              */
+    uint32_t qshift;         /* query rounding shift s (reading #13)              */
+    double sigma_e;          /* BFV error std-dev (3.2, BASELINE.json configs[0]) */
+} ephdc_params;
+
+/* Derived values of a context (for tests and tooling). */
+typedef struct {
+    uint32_t N, L, B, k;     /* B = floor(N/k) queries per ciphertext     */
+    uint64_t t, psi_t;       /* psi_t: minimal primitive 2N-th root mod t (#2)   */
+    uint64_t q[EPHDC_MAX_PRIMES];
+    uint64_t psi[EPHDC_MAX_PRIMES];    /* minimal primitive 2N-th roots mod q_j  */
+    uint64_t delta[EPHDC_MAX_PRIMES];  /* floor(Q/t) mod q_j, Q = prod q_j (#4) */
+    uint32_t fused_split;    /* S: CTAs per polynomial in the fused MAC kernel   */
+    uint32_t fused_chunks;   /* dim chunks per batch in the fused MAC kernel     */
+    int device;              /* CUDA device, -1 for a host-only context          */
+} ephdc_ctx_info;
+
+typedef struct ephdc_ctx ephdc_ctx;
+typedef struct ephdc_sk ephdc_sk;
+typedef struct ephdc_model ephdc_model;
+typedef struct ephdc_workspace ephdc_workspace;
+typedef struct ephdc_ntt_plan ephdc_ntt_plan;
+
+const char *ephdc_status_string(ephdc_status s);
+int ephdc_abi_version(void);
+
+/* ---------------- host helpers (no device needed) ------------------------- */
+
+/* Prime chain of BASELINE.json configs (reading #18): for each bound 2^bits[i],
+ * the largest prime p < 2^bits[i] with p = 1 mod 2N that is not in exclude[]
+ * and not already chosen.  out[count].  EPARAM if bits[i] > 62 or none exists. */
+ephdc_status ephdc_find_ntt_primes(uint32_t log2N, const uint32_t *bits, uint32_t count,
+                                   const uint64_t *exclude, uint32_t n_exclude, uint64_t *out);
+
+/* Minimal primitive 2N-th root of unity mod prime p (reading #2). */
+ephdc_status ephdc_min_psi(uint64_t p, uint32_t log2N, uint64_t *psi);
+
+/* CDT thresholds of the discrete Gaussian sampler (reading #10): out[20]. */
+ephdc_status ephdc_gaussian_cdt(double sigma, uint64_t *out20);
+
+/* Number of CUDA kernels this library has launched in this process (all
+ * entry points).  Used by bench.py for the gpu_launches claim. */
+uint64_t ephdc_launch_count(void);
+
+/* ---------------- context ------------------------------------------------- */
+
+/* Validates params, derives psi, Delta, B, builds the twiddle tables
+ * (bit-reversed psi powers with Shoup companions) and, for device >= 0,
+ * uploads them to that CUDA device.  device = -1 builds a HOST-ONLY context
+ * usable by keygen, sk_export and decrypt_* (tests without a GPU).
+ * Synchronous.  Errors: ENULL, EPARAM, ECUDA, ERESOURCE. */
+ephdc_status ephdc_ctx_create(const ephdc_params *params, int device, ephdc_ctx **out);
+void ephdc_ctx_free(ephdc_ctx *ctx);
+ephdc_status ephdc_ctx_query(const ephdc_ctx *ctx, ephdc_ctx_info *info);
+
+/* ---------------- server side (CS1) ---------------------------- */
+
+/* Secret key: ternary s (reading #9) from SplitMix64 stream (seed, 2,
+ * 0, i) (reading #7), and s_hat_j = NTT_j(s).  Host-only, deterministic. */
+ephdc_status ephdc_keygen(const ephdc_ctx *ctx, uint64_t seed, ephdc_sk **out);
+void ephdc_sk_free(ephdc_sk *sk);
+/* s_out[N] int8 in {-1,0,1}; s_hat_out[L][N] (may be NULL). */
+ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_out);
+
+/* Encrypts the model ("encrypt the class hypervectors"): for
+ * d < D_live, m_d = encode(tile_d), tile_d[i] = class_hv[i mod k][d] mod t for
+ * i < k*B else 0; per prime: c1 = a (uniform in the NTT domain, #6, #8),
+ * c0 = NTT_j([Delta*m_d + e_d]_{q_j}) - a (.) s_hat_j (secret-key BFV, #4, #5;
+ * e_d CDT Gaussian, #10).  class_hv: HOST int8 [k][D_live] with |v| < t/2.
+ * The model lives on the context's device: u64 [D_live][L][2][N].
+ * Synchronous.  Errors: ENULL, ECONTEXT (host-only ctx), ECUDA, ERESOURCE. */
+ephdc_status ephdc_encrypt_model(const ephdc_ctx *ctx, const ephdc_sk *sk, const int8_t *class_hv,
+                                 uint64_t seed, ephdc_model **out);
+void ephdc_model_free(ephdc_model *m);
+/* Copies ciphertexts of dims [d0, d0+nd) to host_out [nd][L][2][N] (canonical).
+ * Synchronous.  EPARAM if d0+nd > D_live. */
+ephdc_status ephdc_model_export(const ephdc_model *m, uint32_t d0, uint32_t nd, uint64_t *host_out);
+
+/* ---------------- client side (the hot path; CS2) ---------------------------- */
+
+/* Device scratch for up to max_nq queries: query/hypervector staging, the
+ * encoded plaintexts of one batch and the scores buffers.  Synchronous. */
+ephdc_status ephdc_workspace_create(const ephdc_ctx *ctx, uint32_t max_nq, ephdc_workspace **out);
+void ephdc_workspace_free(ephdc_workspace *ws);
+/* Per-kernel-class device time (ms, CUDA events on the launching stream) of
+ * the calls since the last reset, when timing is enabled.  names/ms/launches
+ * arrays of length *n (in: capacity, out: count).  Synchronises the workspace's
+ * last stream.  Classes: "encode", "pack_intt", "ntt_mac", "finalize". */
+ephdc_status ephdc_workspace_set_timing(ephdc_workspace *ws, int enable);
+ephdc_status ephdc_workspace_timing(ephdc_workspace *ws, const char **names, double *ms,
+                                    uint64_t *launches, uint32_t *n);
+
+/* HDC encoding + quantisation (BASELINE.json subsystem (a)):
+ * acc[d][q] = sum_f P[d][f] * X[q][f] (exact int32), h = clamp(floor((acc +
+ * 2^(s-1)) / 2^s), +-(2^(Q-1)-1)) for d < D_live, q < nq.
+ * d_X: [nq][F] int8 or uint8 (feat_unsigned); d_P: [D_stored][F] int8 (+-1, or 0);
+ * d_H: [D_live][nq] int8 (dim-major: row d feeds plaintext d).  Async. */
+ephdc_status ephdc_encode_queries(const ephdc_ctx *ctx, const void *d_X, const int8_t *d_P, uint32_t nq,
+                                  int8_t *d_H, void *stream);
+
+/* Unquantised projection acc[d][i] = sum_f P[d][f] X[i][f] (exact int32) for
+ * d < D_live, i < n: the same kernel with a raw epilogue, used server-side to
+ * encode training samples before bundling.  d_acc: [D_live][n]. Async. */
+ephdc_status ephdc_encode_raw(const ephdc_ctx *ctx, const void *d_X, const int8_t *d_P, uint32_t n,
+                              int32_t *d_acc, void *stream);
+
+/* Client evaluation: for each batch b < nb = ceil(nq/B),
+ * d_out[b] = sum_{d < D_live} CT_d (x) NTT(lift(encode(v_{b,d}))) where slot i of
+ * v_{b,d} is h[d][b*B + i/k] mod t for i < k*n_b (n_b = queries in batch b),
+ * else 0 (#19); lift is centered (#3).  d_H: [D_live][nq] int8; d_out:
+ * [cap_ct][2][L][N] u64, canonical NTT form (slot order #1).  EOVERFLOW if
+ * cap_ct < nb, EPARAM if nq > the workspace's max_nq.  Async. */
+ephdc_status ephdc_infer_batch(const ephdc_ctx *ctx, const ephdc_model *model, ephdc_workspace *ws,
+                               const int8_t *d_H, uint32_t nq, uint64_t *d_out, uint32_t cap_ct,
+                               void *stream);
+
+/* Intermediate export for parity tests: the plaintext NTTs p_hat_{b,d,j} of
+ * batch b for dims [d0, d0+nd): d_pt [nd][L][N] canonical.  Async. */
+ephdc_status ephdc_encode_plaintexts(const ephdc_ctx *ctx, ephdc_workspace *ws, const int8_t *d_H,
+                                     uint32_t nq, uint32_t b, uint32_t d0, uint32_t nd, uint64_t *d_pt,
+                                     void *stream);
+
+/* End-to-end client call with HOST buffers: copies h_X [nq][F] host->device,
+ * runs encode_queries + infer_batch, copies the nb scores ciphertexts to
+ * h_out [cap_ct][2][L][N].  d_P stays device-resident.  Synchronous on
+ * `stream`.  h_X / h_out should be pinned for full copy bandwidth. */
+ephdc_status ephdc_classify_host(const ephdc_ctx *ctx, const ephdc_model *model, ephdc_workspace *ws,
+                                 const void *h_X, const int8_t *d_P, uint32_t nq, uint64_t *h_out,
+                                 uint32_t cap_ct, void *stream);
+
+/* ---------------- server decide (test-only host; CS3) ----------------------- */
+
+/* Decrypts nb = ceil(nq/B) scores ciphertexts h_ct [nb][2][L][N]:
+ * x = c0 + c1*s (CRT over the q_j, multi-precision), m = floor((t*x +
+ * floor(Q/2)) / Q) mod t, slots = NTT_t(m), slot i -> (query b*B + i/k,
+ * class i mod k), centered to (-t/2, t/2] (#20).  h_scores [nq][k] int64,
+ * h_labels [nq] = lowest class attaining the max (may be NULL).
+ * Host-only; works on a host-only context. */
+ephdc_status ephdc_decrypt_scores(const ephdc_ctx *ctx, const ephdc_sk *sk, const uint64_t *h_ct,
+                                  uint32_t nq, int64_t *h_scores, uint32_t *h_labels);
+/* Decrypts one ciphertext h_ct [2][L][N] to its N slot values in [0, t). */
+ephdc_status ephdc_decrypt_slots(const ephdc_ctx *ctx, const ephdc_sk *sk, const uint64_t *h_ct,
+                                 uint64_t *h_slots);
+
+/* ---------------- standalone kernels (c5 microbench; CS5) ------------------- */
+
+/* Tables for L primes (each = 1 mod 2N, < 2^61) at ring degree N = 2^log2N,
+ * 10 <= log2N <= 16, on `device`.  Synchronous. */
+ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device,
+                                   ephdc_ntt_plan **out);
+void ephdc_ntt_plan_free(ephdc_ntt_plan *p);
+/* In-place negacyclic NTT of d_polys [batch][L][N] (residues < q_j), natural
+ * coefficient order <-> bit-reversed evaluation order (#1).  Async. */
+ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream);
+ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream);
+/* Pointwise MAC: d_out[j][c][i] = sum_{d<D} d_ct[d][j][c][i] *
+ * d_pt[d][j][i] mod q_j; d_ct [D][L][2][N], d_pt [D][L][N], d_out [L][2][N].
+ * Async (the call zeroes d_out itself). */
+ephdc_status ephdc_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
+                       uint64_t *d_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPHDC_H */

@@ -25,7 +25,7 @@ CDT_LEN = 20          # magnitudes 0..19 (6-sigma cut at sigma = 3.2)
 
 
 def gaussian_cdt(sigma: float = 3.2, n: int = CDT_LEN) -> np.ndarray:
-    """Reading #10: cumulative thresholds T[k] = round(2^48 * cdf(k)) * 2^15, T[n-1] = 2^63.
+    """Reading #10: cumulative thresholds T[k] = round(2^40 * cdf(k)) * 2^23, T[n-1] = 2^63.
 
     p(0) = rho(0)/Z, p(k) = 2 rho(k)/Z (k >= 1), rho(x) = exp(-x^2 / (2 sigma^2)),
     Z = rho(0) + 2 sum_{k=1}^{n-1} rho(k).  Evaluated with 50-digit decimals.
@@ -38,8 +38,8 @@ def gaussian_cdt(sigma: float = 3.2, n: int = CDT_LEN) -> np.ndarray:
     out, acc = [], Decimal(0)
     for k in range(n):
         acc += w[k]
-        v = acc / Z * (Decimal(2) ** 48)
-        out.append(int(v.to_integral_value(rounding="ROUND_HALF_EVEN")) << 15)
+        v = acc / Z * (Decimal(2) ** 40)
+        out.append(int(v.to_integral_value(rounding="ROUND_HALF_EVEN")) << 23)
     out[-1] = 1 << 63
     return np.array(out, dtype=np.uint64)
 

@@ -1,0 +1,305 @@
+"""paper_2511_00737_b200 -- B200 (sm_100a) hot path of EP-HDC client-side encrypted HDC inference.
+
+Python layer over libephdc.so (include/ephdc.h).  PyTorch supplies device memory
+and streams; every step of the path runs in the library's CUDA kernels.  Names
+follow the C ABI: Context (ephdc_ctx_*), SecretKey (ephdc_keygen), EncryptedModel
+(ephdc_encrypt_model), Workspace (ephdc_workspace_*), encode_queries,
+infer_batch, decrypt_scores, NttPlan (ephdc_ntt_*), mac.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _capi
+from ._capi import EphdcError, call, lib
+
+__all__ = [
+    "Context", "SecretKey", "EncryptedModel", "Workspace", "NttPlan", "EphdcError",
+    "find_ntt_primes", "min_psi", "gaussian_cdt", "launch_count",
+    "encode_queries", "encode_raw", "infer_batch", "encode_plaintexts", "classify_host",
+    "decrypt_scores", "decrypt_slots", "ntt_fwd", "ntt_inv", "mac",
+]
+
+
+def _np_ptr(a: np.ndarray) -> int:
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def _dptr(t) -> int:
+    """Device pointer of a contiguous CUDA torch tensor."""
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    return t.data_ptr()
+
+
+def _stream(stream=None) -> Optional[int]:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def launch_count() -> int:
+    return _capi.launch_count()
+
+
+# --------------------------------------------------------------------------- host helpers
+def find_ntt_primes(log2N: int, bits: Sequence[int], exclude: Sequence[int] = ()) -> list:
+    b = np.ascontiguousarray(np.array(bits, dtype=np.uint32))
+    ex = np.ascontiguousarray(np.array(list(exclude) or [0], dtype=np.uint64))
+    out = np.zeros(len(bits), dtype=np.uint64)
+    call("ephdc_find_ntt_primes", log2N, _np_ptr(b), len(bits), _np_ptr(ex), len(exclude), _np_ptr(out))
+    return [int(x) for x in out]
+
+
+def min_psi(p: int, log2N: int) -> int:
+    out = ctypes.c_uint64()
+    call("ephdc_min_psi", p, log2N, ctypes.addressof(out))
+    return int(out.value)
+
+
+def gaussian_cdt(sigma: float = 3.2) -> np.ndarray:
+    out = np.zeros(20, dtype=np.uint64)
+    call("ephdc_gaussian_cdt", sigma, _np_ptr(out))
+    return out
+
+
+# --------------------------------------------------------------------------- handles
+class Context:
+    """ephdc_ctx: parameters, twiddle tables, device constants."""
+
+    def __init__(self, *, log2N: int, q: Sequence[int], t: int, k: int, D_live: int, D_stored: int, F: int,
+                 feat_unsigned: bool, Qbits: int, Cbits: int, qshift: int, sigma_e: float = 3.2,
+                 device: int = 0):
+        self._q = np.ascontiguousarray(np.array(q, dtype=np.uint64))
+        self.params = _capi.Params(log2N, len(q), self._q.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), t, k,
+                                   D_live, D_stored, F, int(feat_unsigned), Qbits, Cbits, qshift, sigma_e)
+        self._h = ctypes.c_void_p()
+        call("ephdc_ctx_create", ctypes.byref(self.params), device, ctypes.byref(self._h))
+        info = _capi.CtxInfo()
+        call("ephdc_ctx_query", self._h, ctypes.byref(info))
+        self.info = info
+        self.N, self.L, self.B, self.k = info.N, info.L, info.B, info.k
+        self.t, self.psi_t = int(info.t), int(info.psi_t)
+        self.q = [int(info.q[j]) for j in range(self.L)]
+        self.psi = [int(info.psi[j]) for j in range(self.L)]
+        self.delta = [int(info.delta[j]) for j in range(self.L)]
+        self.D_live, self.D_stored, self.F = D_live, D_stored, F
+        self.feat_unsigned = bool(feat_unsigned)
+        self.Qbits, self.Cbits, self.qshift = Qbits, Cbits, qshift
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def n_batches(self, nq: int) -> int:
+        return (nq + self.B - 1) // self.B
+
+    def ct_shape(self, nq: int) -> Tuple[int, int, int, int]:
+        return (self.n_batches(nq), 2, self.L, self.N)
+
+    def close(self):
+        if self._h:
+            lib.ephdc_ctx_free(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SecretKey:
+    def __init__(self, ctx: Context, seed: int):
+        self.ctx = ctx
+        self._h = ctypes.c_void_p()
+        call("ephdc_keygen", ctx.handle, seed, ctypes.byref(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export(self) -> Tuple[np.ndarray, np.ndarray]:
+        s = np.zeros(self.ctx.N, dtype=np.int8)
+        sh = np.zeros((self.ctx.L, self.ctx.N), dtype=np.uint64)
+        call("ephdc_sk_export", self._h, _np_ptr(s), _np_ptr(sh))
+        return s, sh
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.ephdc_sk_free(self._h)
+        except Exception:
+            pass
+
+
+class EncryptedModel:
+    """ephdc_model: D_live NTT-form ciphertexts resident on the device."""
+
+    def __init__(self, ctx: Context, sk: SecretKey, class_hv: np.ndarray, seed: int):
+        C = np.ascontiguousarray(class_hv, dtype=np.int8)
+        if C.shape != (ctx.k, ctx.D_live):
+            raise ValueError(f"class_hv must be [k, D_live] = {(ctx.k, ctx.D_live)}")
+        self.ctx = ctx
+        self._h = ctypes.c_void_p()
+        call("ephdc_encrypt_model", ctx.handle, sk.handle, _np_ptr(C), seed, ctypes.byref(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export(self, d0: int, nd: int) -> np.ndarray:
+        out = np.zeros((nd, self.ctx.L, 2, self.ctx.N), dtype=np.uint64)
+        call("ephdc_model_export", self._h, d0, nd, _np_ptr(out))
+        return out
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.ephdc_model_free(self._h)
+        except Exception:
+            pass
+
+
+class Workspace:
+    def __init__(self, ctx: Context, max_nq: int):
+        self.ctx = ctx
+        self.max_nq = max_nq
+        self._h = ctypes.c_void_p()
+        call("ephdc_workspace_create", ctx.handle, max_nq, ctypes.byref(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_timing(self, enable: bool) -> None:
+        call("ephdc_workspace_set_timing", self._h, int(enable))
+
+    def timing(self) -> Dict[str, Tuple[float, int]]:
+        n = ctypes.c_uint32(8)
+        names = (ctypes.c_char_p * 8)()
+        ms = np.zeros(8, dtype=np.float64)
+        cnt = np.zeros(8, dtype=np.uint64)
+        call("ephdc_workspace_timing", self._h, ctypes.addressof(names), _np_ptr(ms), _np_ptr(cnt), ctypes.byref(n))
+        return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.ephdc_workspace_free(self._h)
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------------- client hot path
+def encode_queries(ctx: Context, X, P, H=None, stream=None):
+    """X: cuda [nq, F] int8/uint8, P: cuda [D_stored, F] int8 -> H cuda [D_live, nq] int8."""
+    import torch
+    nq = X.shape[0]
+    if H is None:
+        H = torch.empty((ctx.D_live, nq), dtype=torch.int8, device=X.device)
+    call("ephdc_encode_queries", ctx.handle, _dptr(X), _dptr(P), nq, _dptr(H), _stream(stream))
+    return H
+
+
+def encode_raw(ctx: Context, X, P, out=None, stream=None):
+    """Unquantised int32 projection acc[d][n] (server-side training; same kernel, RAW epilogue)."""
+    import torch
+    n = X.shape[0]
+    if out is None:
+        out = torch.empty((ctx.D_live, n), dtype=torch.int32, device=X.device)
+    call("ephdc_encode_raw", ctx.handle, _dptr(X), _dptr(P), n, _dptr(out), _stream(stream))
+    return out
+
+
+def infer_batch(ctx: Context, model: EncryptedModel, ws: Workspace, H, nq: Optional[int] = None, out=None,
+                stream=None):
+    """H: cuda [D_live, nq] int8 -> scores ciphertexts cuda [nb, 2, L, N] uint64 (as int64 storage)."""
+    import torch
+    nq = H.shape[1] if nq is None else nq
+    if out is None:
+        out = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, device=H.device)
+    call("ephdc_infer_batch", ctx.handle, model.handle, ws.handle, _dptr(H), nq, _dptr(out), out.shape[0],
+         _stream(stream))
+    return out
+
+
+def encode_plaintexts(ctx: Context, ws: Workspace, H, b: int, d0: int, nd: int, out=None, stream=None):
+    import torch
+    nq = H.shape[1]
+    if out is None:
+        out = torch.empty((nd, ctx.L, ctx.N), dtype=torch.int64, device=H.device)
+    call("ephdc_encode_plaintexts", ctx.handle, ws.handle, _dptr(H), nq, b, d0, nd, _dptr(out), _stream(stream))
+    return out
+
+
+def classify_host(ctx: Context, model: EncryptedModel, ws: Workspace, X_host, P, out_host=None, stream=None):
+    """End-to-end call with host buffers (X_host: pinned CPU tensor [nq, F]; returns CPU [nb,2,L,N])."""
+    import torch
+    nq = X_host.shape[0]
+    if out_host is None:
+        out_host = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, pin_memory=True)
+    call("ephdc_classify_host", ctx.handle, model.handle, ws.handle, X_host.data_ptr(), _dptr(P), nq,
+         out_host.data_ptr(), out_host.shape[0], _stream(stream))
+    return out_host
+
+
+# --------------------------------------------------------------------------- server decide (host)
+def decrypt_scores(ctx: Context, sk: SecretKey, cts: np.ndarray, nq: int) -> Tuple[np.ndarray, np.ndarray]:
+    c = np.ascontiguousarray(cts, dtype=np.uint64)
+    scores = np.zeros((nq, ctx.k), dtype=np.int64)
+    labels = np.zeros(nq, dtype=np.uint32)
+    call("ephdc_decrypt_scores", ctx.handle, sk.handle, _np_ptr(c), nq, _np_ptr(scores), _np_ptr(labels))
+    return scores, labels
+
+
+def decrypt_slots(ctx: Context, sk: SecretKey, ct: np.ndarray) -> np.ndarray:
+    c = np.ascontiguousarray(ct, dtype=np.uint64)
+    out = np.zeros(ctx.N, dtype=np.uint64)
+    call("ephdc_decrypt_slots", ctx.handle, sk.handle, _np_ptr(c), _np_ptr(out))
+    return out
+
+
+# --------------------------------------------------------------------------- standalone (c5)
+class NttPlan:
+    def __init__(self, q: Sequence[int], log2N: int, device: int = 0):
+        self.q = [int(x) for x in q]
+        self.L, self.log2N, self.N = len(q), log2N, 1 << log2N
+        qa = np.ascontiguousarray(np.array(self.q, dtype=np.uint64))
+        self._h = ctypes.c_void_p()
+        call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device, ctypes.byref(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.ephdc_ntt_plan_free(self._h)
+        except Exception:
+            pass
+
+
+def ntt_fwd(plan: NttPlan, polys, stream=None):
+    call("ephdc_ntt_fwd", plan.handle, _dptr(polys), polys.numel() // (plan.L * plan.N), _stream(stream))
+    return polys
+
+
+def ntt_inv(plan: NttPlan, polys, stream=None):
+    call("ephdc_ntt_inv", plan.handle, _dptr(polys), polys.numel() // (plan.L * plan.N), _stream(stream))
+    return polys
+
+
+def mac(plan: NttPlan, ct, pt, out=None, stream=None):
+    import torch
+    D = pt.shape[0]
+    if out is None:
+        out = torch.empty((plan.L, 2, plan.N), dtype=torch.int64, device=pt.device)
+    call("ephdc_mac", plan.handle, _dptr(ct), _dptr(pt), D, _dptr(out), _stream(stream))
+    return out

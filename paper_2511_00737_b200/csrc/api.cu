@@ -1,0 +1,658 @@
+// api.cu -- implementation of the C ABI declared in include/ephdc.h.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+#include "rng.cuh"
+
+using namespace ephdc;
+using namespace ephdc_host;
+
+namespace {
+
+#define EPHDC_CUDA_TRY(expr)                     \
+    do {                                         \
+        cudaError_t _e = (expr);                 \
+        if (_e != cudaSuccess) return EPHDC_ECUDA; \
+    } while (0)
+
+const char *kClassNames[ephdc_workspace::kClasses] = {"encode", "pack_intt", "ntt_mac", "finalize"};
+enum { kClsEncode = 0, kClsPack = 1, kClsMac = 2, kClsFinal = 3 };
+
+template <class T> cudaError_t dev_alloc(T **p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void **>(p), sizeof(T) * (n ? n : 1));
+}
+
+// RAII device buffer for temporaries
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+};
+
+// Timed launch helper for the workspace instrumentation.
+struct Timer {
+    ephdc_workspace *ws;
+    cudaStream_t st;
+    int cls;
+    int idx = -1;
+    Timer(ephdc_workspace *w, cudaStream_t s, int c) : ws(w), st(s), cls(c) {
+        if (ws && ws->timing) {
+            size_t need = ws->ev_marks.size() * 2 + 2;
+            while (ws->ev_pool.size() < need) {
+                cudaEvent_t e;
+                if (cudaEventCreate(&e) != cudaSuccess) return;
+                ws->ev_pool.push_back(e);
+            }
+            idx = (int)ws->ev_marks.size() * 2;
+            cudaEventRecord(ws->ev_pool[idx], st);
+        }
+    }
+    void done() {
+        if (idx >= 0) {
+            cudaEventRecord(ws->ev_pool[idx + 1], st);
+            ws->ev_marks.push_back({cls, idx});
+            ws->launches[cls] += 1;
+            idx = -1;
+        }
+    }
+};
+
+bool is_ntt_prime(uint64_t p, uint32_t log2N) { return p > 2 && (p - 1) % (2ull << log2N) == 0 && is_prime_u64(p); }
+
+uint64_t mask_for(uint64_t q) {
+    uint64_t m = 1;
+    while (m < q) m = (m << 1) | 1;
+    return m;
+}
+
+void fill_prime_set(PrimeSet &ps, const std::vector<uint64_t> &q, uint64_t t) {
+    memset(&ps, 0, sizeof(ps));
+    for (size_t j = 0; j < q.size(); ++j) {
+        ps.q[j] = q[j];
+        ps.qinv[j] = inv_mod_2_64(q[j]);
+        ps.r2[j] = two128_mod(q[j]);
+        ps.qmt[j] = t ? q[j] - t : 0;
+        ps.mask[j] = mask_for(q[j]);
+    }
+}
+
+std::vector<TwPair<u64>> make_tw64(uint64_t psi, uint64_t p, uint32_t log2N) {
+    const uint32_t N = 1u << log2N;
+    std::vector<uint64_t> pw(N);
+    pow_brev(psi, p, log2N, pw.data());
+    std::vector<TwPair<u64>> out(N);
+    for (uint32_t i = 0; i < N; ++i) out[i] = TwPair<u64>{pw[i], shoup64(pw[i], p)};
+    return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ephdc_status_string(ephdc_status s) {
+    switch (s) {
+        case EPHDC_OK: return "ok";
+        case EPHDC_EPARAM: return "invalid parameter";
+        case EPHDC_ECONTEXT: return "context mismatch or host-only context";
+        case EPHDC_EOVERFLOW: return "output capacity too small";
+        case EPHDC_ERESOURCE: return "allocation failed";
+        case EPHDC_ECUDA: return "CUDA error";
+        case EPHDC_EDOMAIN: return "value outside its modular domain";
+        case EPHDC_ENULL: return "null pointer";
+    }
+    return "unknown status";
+}
+
+int ephdc_abi_version(void) { return EPHDC_ABI_VERSION; }
+
+uint64_t ephdc_launch_count(void) { return g_launches.load(); }
+
+ephdc_status ephdc_find_ntt_primes(uint32_t log2N, const uint32_t *bits, uint32_t count, const uint64_t *exclude,
+                                   uint32_t n_exclude, uint64_t *out) {
+    if (!bits || !out || (n_exclude && !exclude)) return EPHDC_ENULL;
+    if (log2N < 1 || log2N > 20) return EPHDC_EPARAM;
+    return ntt_prime_chain(log2N, bits, count, exclude, n_exclude, out) ? EPHDC_OK : EPHDC_EPARAM;
+}
+
+ephdc_status ephdc_min_psi(uint64_t p, uint32_t log2N, uint64_t *psi) {
+    if (!psi) return EPHDC_ENULL;
+    if (log2N > 20 || !is_ntt_prime(p, log2N)) return EPHDC_EPARAM;
+    *psi = min_primitive_root_2n(p, log2N);
+    return *psi ? EPHDC_OK : EPHDC_EPARAM;
+}
+
+ephdc_status ephdc_gaussian_cdt(double sigma, uint64_t *out20) {
+    if (!out20) return EPHDC_ENULL;
+    if (!(sigma > 0.0) || sigma > 100.0) return EPHDC_EPARAM;
+    gaussian_cdt(sigma, out20);
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// context
+// ------------------------------------------------------------------------------------
+void ephdc_ctx_free(ephdc_ctx *c) {
+    if (!c) return;
+    if (c->device >= 0) {
+        cudaSetDevice(c->device);
+        cudaFree(c->dev.tw_q);
+        cudaFree(c->dev.itw_t);
+        cudaFree(c->dev.cdt);
+    }
+    delete c;
+}
+
+ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out) {
+    if (!p || !out || !p->q) return EPHDC_ENULL;
+    *out = nullptr;
+    if (p->log2N < 10 || p->log2N > 14 || p->L < 1 || p->L > EPHDC_MAX_PRIMES) return EPHDC_EPARAM;
+    const uint32_t N = 1u << p->log2N;
+    if (p->k < 1 || p->k > N || p->D_live < 1 || p->D_stored < p->D_live || p->F < 4 || p->F % 4) return EPHDC_EPARAM;
+    if (p->Qbits < 2 || p->Qbits > 8 || p->Cbits < 2 || p->Cbits > 8 || p->qshift > 30) return EPHDC_EPARAM;
+    if (!(p->sigma_e > 0.0) || p->sigma_e > 100.0) return EPHDC_EPARAM;
+    if (p->t >= (1ull << 30) || !is_ntt_prime(p->t, p->log2N)) return EPHDC_EPARAM;
+    for (uint32_t j = 0; j < p->L; ++j) {
+        if (p->q[j] >= (1ull << 60) || p->q[j] <= p->t || !is_ntt_prime(p->q[j], p->log2N)) return EPHDC_EPARAM;
+        for (uint32_t i = 0; i < j; ++i)
+            if (p->q[i] == p->q[j]) return EPHDC_EPARAM;
+    }
+    std::unique_ptr<ephdc_ctx> c(new (std::nothrow) ephdc_ctx());
+    if (!c) return EPHDC_ERESOURCE;
+    c->p = *p;
+    c->q.assign(p->q, p->q + p->L);
+    c->p.q = c->q.data();
+    c->N = N;
+    c->L = p->L;
+    c->t = p->t;
+    c->B = N / p->k;
+    c->psi_t = min_primitive_root_2n(p->t, p->log2N);
+    if (!c->psi_t) return EPHDC_EPARAM;
+    for (uint64_t qj : c->q) {
+        uint64_t ps = min_primitive_root_2n(qj, p->log2N);
+        if (!ps) return EPHDC_EPARAM;
+        c->psi.push_back(ps);
+    }
+    // Delta = floor(Q / t) (reading #4), reduced per prime
+    Big Q = big_from_product(c->q);
+    Big delta = big_div_small(Q, p->t, nullptr);
+    fill_prime_set(c->ps, c->q, p->t);
+    for (uint32_t j = 0; j < c->L; ++j) {
+        c->delta.push_back(big_mod_small(delta, c->q[j]));
+        c->ps.delta[j] = c->delta[j];
+        c->ps.delta_p[j] = shoup64(c->delta[j], c->q[j]);
+    }
+    const uint32_t ninv = (uint32_t)invmod(N % p->t, p->t);
+    c->ninv_t = ninv;
+    c->ninv_t_p = shoup32(ninv, (uint32_t)p->t);
+    gaussian_cdt(p->sigma_e, c->cdt);
+    c->host_q.resize(c->L);
+    for (uint32_t j = 0; j < c->L; ++j) c->host_q[j].init(c->q[j], c->psi[j], p->log2N);
+    c->host_t.init(p->t, c->psi_t, p->log2N);
+    c->crt.init(c->q, p->t);
+    // fused MAC kernel geometry: S CTAs per polynomial (N = 16384 -> 2 halves of 8192),
+    // dims split in chunks so the grid holds ~8 waves; all partial sums < 2^64.
+    c->fused_S = p->log2N >= 14 ? (1u << (p->log2N - 13)) : 1u;
+    {
+        const uint32_t occ = (uint32_t)ntt_mac_occupancy(p->log2N, c->fused_S);
+        const uint64_t target = 8ull * 148 * occ;
+        uint64_t chunks = (target + c->L * c->fused_S - 1) / (c->L * c->fused_S);
+        chunks = std::max<uint64_t>(1, std::min<uint64_t>(chunks, p->D_live));
+        uint64_t qmax = *std::max_element(c->q.begin(), c->q.end());
+        chunks = std::min<uint64_t>(chunks, ~0ull / qmax);
+        c->fused_G = (uint32_t)((p->D_live + chunks - 1) / chunks);
+        c->fused_chunks = (p->D_live + c->fused_G - 1) / c->fused_G;
+    }
+    c->device = device;
+    if (device >= 0) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) return EPHDC_ECUDA;
+        EPHDC_CUDA_TRY(cudaSetDevice(device));
+        std::vector<TwPair<u64>> twq((size_t)c->L * N);
+        for (uint32_t j = 0; j < c->L; ++j) {
+            auto tj = make_tw64(c->psi[j], c->q[j], p->log2N);
+            std::copy(tj.begin(), tj.end(), twq.begin() + (size_t)j * N);
+        }
+        std::vector<uint64_t> ipw(N);
+        pow_brev(invmod(c->psi_t, p->t), p->t, p->log2N, ipw.data());
+        std::vector<TwPair<u32>> itw(N);
+        for (uint32_t i = 0; i < N; ++i) itw[i] = TwPair<u32>{(u32)ipw[i], shoup32((u32)ipw[i], (u32)p->t)};
+        if (dev_alloc(&c->dev.tw_q, twq.size()) != cudaSuccess || dev_alloc(&c->dev.itw_t, itw.size()) != cudaSuccess ||
+            dev_alloc(&c->dev.cdt, 20) != cudaSuccess) {
+            ephdc_ctx_free(c.release());
+            return EPHDC_ERESOURCE;
+        }
+        if (cudaMemcpy(c->dev.tw_q, twq.data(), sizeof(twq[0]) * twq.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->dev.itw_t, itw.data(), sizeof(itw[0]) * itw.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->dev.cdt, c->cdt, sizeof(c->cdt), cudaMemcpyHostToDevice) != cudaSuccess) {
+            ephdc_ctx_free(c.release());
+            return EPHDC_ECUDA;
+        }
+    }
+    *out = c.release();
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_ctx_query(const ephdc_ctx *c, ephdc_ctx_info *info) {
+    if (!c || !info) return EPHDC_ENULL;
+    memset(info, 0, sizeof(*info));
+    info->N = c->N;
+    info->L = c->L;
+    info->B = c->B;
+    info->k = c->p.k;
+    info->t = c->t;
+    info->psi_t = c->psi_t;
+    for (uint32_t j = 0; j < c->L; ++j) {
+        info->q[j] = c->q[j];
+        info->psi[j] = c->psi[j];
+        info->delta[j] = c->delta[j];
+    }
+    info->fused_split = c->fused_S;
+    info->fused_chunks = c->fused_chunks;
+    info->device = c->device;
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// keys and model
+// ------------------------------------------------------------------------------------
+ephdc_status ephdc_keygen(const ephdc_ctx *c, uint64_t seed, ephdc_sk **out) {
+    if (!c || !out) return EPHDC_ENULL;
+    std::unique_ptr<ephdc_sk> sk(new (std::nothrow) ephdc_sk());
+    if (!sk) return EPHDC_ERESOURCE;
+    sk->ctx = c;
+    const uint32_t N = c->N;
+    sk->s.resize(N);
+    for (uint32_t i = 0; i < N; ++i) sk->s[i] = (int8_t)ephdc_rng::ternary(seed, i);
+    sk->s_hat.resize((size_t)c->L * N);
+    for (uint32_t j = 0; j < c->L; ++j) {
+        uint64_t *sh = sk->s_hat.data() + (size_t)j * N;
+        for (uint32_t i = 0; i < N; ++i) sh[i] = sk->s[i] < 0 ? c->q[j] - 1 : (uint64_t)sk->s[i];
+        c->host_q[j].forward(sh);
+    }
+    *out = sk.release();
+    return EPHDC_OK;
+}
+
+void ephdc_sk_free(ephdc_sk *sk) { delete sk; }
+
+ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_out) {
+    if (!sk || !s_out) return EPHDC_ENULL;
+    memcpy(s_out, sk->s.data(), sk->s.size());
+    if (s_hat_out) memcpy(s_hat_out, sk->s_hat.data(), sizeof(uint64_t) * sk->s_hat.size());
+    return EPHDC_OK;
+}
+
+void ephdc_model_free(ephdc_model *m) {
+    if (!m) return;
+    if (m->d_ct) {
+        cudaSetDevice(m->ctx->device);
+        cudaFree(m->d_ct);
+    }
+    delete m;
+}
+
+ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const int8_t *class_hv, uint64_t seed,
+                                 ephdc_model **out) {
+    if (!c || !sk || !class_hv || !out) return EPHDC_ENULL;
+    *out = nullptr;
+    if (sk->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    const uint32_t N = c->N, L = c->L, D = c->p.D_live, k = c->p.k;
+    for (size_t i = 0; i < (size_t)k * D; ++i)
+        if (2 * (int64_t)(class_hv[i] < 0 ? -class_hv[i] : class_hv[i]) >= (int64_t)c->t) return EPHDC_EDOMAIN;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    std::unique_ptr<ephdc_model> m(new (std::nothrow) ephdc_model());
+    if (!m) return EPHDC_ERESOURCE;
+    m->ctx = c;
+    m->D = D;
+    if (dev_alloc(&m->d_ct, (size_t)D * L * 2 * N) != cudaSuccess) return EPHDC_ERESOURCE;
+    // s_hat in Montgomery form (s_hat * 2^64 mod q): mont_mul(a, s_hat*2^64) = a * s_hat
+    std::vector<uint64_t> shm((size_t)L * N);
+    for (uint32_t j = 0; j < L; ++j) {
+        const uint64_t r = (uint64_t)(((u128)1 << 64) % c->q[j]);
+        for (uint32_t i = 0; i < N; ++i) shm[(size_t)j * N + i] = mulmod(sk->s_hat[(size_t)j * N + i], r, c->q[j]);
+    }
+    const uint32_t chunk = std::min<uint32_t>(D, 2048);
+    DevBuf bC, bS, bM;
+    if (cudaMalloc(&bC.p, (size_t)k * D) != cudaSuccess || cudaMalloc(&bS.p, sizeof(uint64_t) * shm.size()) != cudaSuccess ||
+        cudaMalloc(&bM.p, sizeof(uint32_t) * (size_t)chunk * N) != cudaSuccess)
+        return EPHDC_ERESOURCE;
+    EPHDC_CUDA_TRY(cudaMemcpy(bC.p, class_hv, (size_t)k * D, cudaMemcpyHostToDevice));
+    EPHDC_CUDA_TRY(cudaMemcpy(bS.p, shm.data(), sizeof(uint64_t) * shm.size(), cudaMemcpyHostToDevice));
+    cudaStream_t st = 0;
+    for (uint32_t d0 = 0; d0 < D; d0 += chunk) {
+        const uint32_t nd = std::min(chunk, D - d0);
+        EPHDC_CUDA_TRY(launch_pack_intt_model(c, (const int8_t *)bC.p, d0, nd, (uint32_t *)bM.p, st));
+        EPHDC_CUDA_TRY(launch_encrypt(c, (const uint32_t *)bM.p, d0, nd, (const uint64_t *)bS.p, seed, m->d_ct, st));
+    }
+    EPHDC_CUDA_TRY(cudaDeviceSynchronize());
+    *out = m.release();
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_model_export(const ephdc_model *m, uint32_t d0, uint32_t nd, uint64_t *host_out) {
+    if (!m || !host_out) return EPHDC_ENULL;
+    if ((uint64_t)d0 + nd > m->D) return EPHDC_EPARAM;
+    const ephdc_ctx *c = m->ctx;
+    const size_t per = (size_t)c->L * 2 * c->N;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    EPHDC_CUDA_TRY(cudaMemcpy(host_out, m->d_ct + per * d0, sizeof(uint64_t) * per * nd, cudaMemcpyDeviceToHost));
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// workspace
+// ------------------------------------------------------------------------------------
+void ephdc_workspace_free(ephdc_workspace *ws) {
+    if (!ws) return;
+    cudaSetDevice(ws->ctx->device);
+    cudaFree(ws->d_M);
+    cudaFree(ws->d_X);
+    cudaFree(ws->d_H);
+    cudaFree(ws->d_out);
+    for (cudaEvent_t e : ws->ev_pool) cudaEventDestroy(e);
+    delete ws;
+}
+
+ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_workspace **out) {
+    if (!c || !out) return EPHDC_ENULL;
+    *out = nullptr;
+    if (c->device < 0) return EPHDC_ECONTEXT;
+    if (max_nq == 0) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    std::unique_ptr<ephdc_workspace> ws(new (std::nothrow) ephdc_workspace());
+    if (!ws) return EPHDC_ERESOURCE;
+    ws->ctx = c;
+    ws->max_nq = max_nq;
+    ws->nb_max = (max_nq + c->B - 1) / c->B;
+    const size_t D = c->p.D_live;
+    if (dev_alloc(&ws->d_M, D * c->N) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
+        dev_alloc(&ws->d_H, D * max_nq) != cudaSuccess ||
+        dev_alloc(&ws->d_out, (size_t)ws->nb_max * 2 * c->L * c->N) != cudaSuccess) {
+        ephdc_workspace_free(ws.release());
+        return EPHDC_ERESOURCE;
+    }
+    *out = ws.release();
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_workspace_set_timing(ephdc_workspace *ws, int enable) {
+    if (!ws) return EPHDC_ENULL;
+    ws->timing = enable != 0;
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_workspace_timing(ephdc_workspace *ws, const char **names, double *ms, uint64_t *launches,
+                                    uint32_t *n) {
+    if (!ws || !n) return EPHDC_ENULL;
+    EPHDC_CUDA_TRY(cudaSetDevice(ws->ctx->device));
+    if (!ws->ev_marks.empty()) {
+        EPHDC_CUDA_TRY(cudaEventSynchronize(ws->ev_pool[ws->ev_marks.back().second + 1]));
+        for (auto &mk : ws->ev_marks) {
+            float e = 0;
+            EPHDC_CUDA_TRY(cudaEventElapsedTime(&e, ws->ev_pool[mk.second], ws->ev_pool[mk.second + 1]));
+            ws->ms[mk.first] += e;
+        }
+        ws->ev_marks.clear();
+    }
+    const uint32_t cnt = std::min<uint32_t>(*n, ephdc_workspace::kClasses);
+    for (uint32_t i = 0; i < cnt; ++i) {
+        if (names) names[i] = kClassNames[i];
+        if (ms) ms[i] = ws->ms[i];
+        if (launches) launches[i] = ws->launches[i];
+        ws->ms[i] = 0;
+        ws->launches[i] = 0;
+    }
+    *n = cnt;
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// client hot path
+// ------------------------------------------------------------------------------------
+static ephdc_status encode_impl(const ephdc_ctx *c, ephdc_workspace *ws, const void *d_X, const int8_t *d_P,
+                                uint32_t nq, int8_t *d_H, cudaStream_t st) {
+    if (nq == 0) return EPHDC_OK;
+    Timer tm(ws, st, kClsEncode);
+    EPHDC_CUDA_TRY(launch_encode(c, d_X, d_P, nq, d_H, false, st));
+    tm.done();
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_encode_queries(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, int8_t *d_H,
+                                  void *stream) {
+    if (!c || ((!d_X || !d_P || !d_H) && nq)) return EPHDC_ENULL;
+    if (c->device < 0) return EPHDC_ECONTEXT;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    return encode_impl(c, nullptr, d_X, d_P, nq, d_H, (cudaStream_t)stream);
+}
+
+ephdc_status ephdc_encode_raw(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t n, int32_t *d_acc,
+                              void *stream) {
+    if (!c || ((!d_X || !d_P || !d_acc) && n)) return EPHDC_ENULL;
+    if (c->device < 0) return EPHDC_ECONTEXT;
+    if (n == 0) return EPHDC_OK;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    EPHDC_CUDA_TRY(launch_encode(c, d_X, d_P, n, d_acc, true, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws, const int8_t *d_H,
+                               uint32_t nq, uint64_t *d_out, cudaStream_t st) {
+    const uint32_t nb = (nq + c->B - 1) / c->B;
+    const size_t per = (size_t)2 * c->L * c->N;
+    if (nb == 0) return EPHDC_OK;
+    EPHDC_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(uint64_t) * per * nb, st));
+    for (uint32_t b = 0; b < nb; ++b) {
+        {
+            Timer tm(ws, st, kClsPack);
+            EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, 0, c->p.D_live, ws->d_M, st));
+            tm.done();
+        }
+        {
+            Timer tm(ws, st, kClsMac);
+            EPHDC_CUDA_TRY(launch_ntt_mac(c, ws->d_M, m->d_ct, d_out + per * b, st));
+            tm.done();
+        }
+        {
+            Timer tm(ws, st, kClsFinal);
+            EPHDC_CUDA_TRY(launch_finalize(c, d_out + per * b, st));
+            tm.done();
+        }
+    }
+    ws->last_stream = st;
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_infer_batch(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws, const int8_t *d_H,
+                               uint32_t nq, uint64_t *d_out, uint32_t cap_ct, void *stream) {
+    if (!c || !m || !ws || ((!d_H || !d_out) && nq)) return EPHDC_ENULL;
+    if (m->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    const uint32_t nb = (nq + c->B - 1) / c->B;
+    if (cap_ct < nb) return EPHDC_EOVERFLOW;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    return infer_impl(c, m, ws, d_H, nq, d_out, (cudaStream_t)stream);
+}
+
+ephdc_status ephdc_encode_plaintexts(const ephdc_ctx *c, ephdc_workspace *ws, const int8_t *d_H, uint32_t nq,
+                                     uint32_t b, uint32_t d0, uint32_t nd, uint64_t *d_pt, void *stream) {
+    if (!c || !ws || !d_H || !d_pt) return EPHDC_ENULL;
+    if (ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    if ((uint64_t)b * c->B >= nq || (uint64_t)d0 + nd > c->p.D_live) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, d0, nd, ws->d_M, st));
+    EPHDC_CUDA_TRY(launch_plaintext_ntt(c, ws->d_M, nd, d_pt, st));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_classify_host(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws, const void *h_X,
+                                 const int8_t *d_P, uint32_t nq, uint64_t *h_out, uint32_t cap_ct, void *stream) {
+    if (!c || !m || !ws || ((!h_X || !d_P || !h_out) && nq)) return EPHDC_ENULL;
+    if (m->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    if (nq > ws->max_nq) return EPHDC_EPARAM;
+    const uint32_t nb = (nq + c->B - 1) / c->B;
+    if (cap_ct < nb) return EPHDC_EOVERFLOW;
+    if (nq == 0) return EPHDC_OK;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    EPHDC_CUDA_TRY(cudaMemcpyAsync(ws->d_X, h_X, (size_t)nq * c->p.F, cudaMemcpyHostToDevice, st));
+    ephdc_status s = encode_impl(c, ws, ws->d_X, d_P, nq, ws->d_H, st);
+    if (s != EPHDC_OK) return s;
+    s = infer_impl(c, m, ws, ws->d_H, nq, ws->d_out, st);
+    if (s != EPHDC_OK) return s;
+    EPHDC_CUDA_TRY(cudaMemcpyAsync(h_out, ws->d_out, sizeof(uint64_t) * 2 * c->L * c->N * nb, cudaMemcpyDeviceToHost, st));
+    EPHDC_CUDA_TRY(cudaStreamSynchronize(st));
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// server decide (host)
+// ------------------------------------------------------------------------------------
+static void decrypt_one(const ephdc_ctx *c, const ephdc_sk *sk, const uint64_t *ct, uint64_t *slots) {
+    const uint32_t N = c->N, L = c->L;
+    std::vector<uint64_t> x((size_t)L * N);
+    for (uint32_t j = 0; j < L; ++j) {
+        const uint64_t q = c->q[j];
+        const uint64_t *c0 = ct + (size_t)j * N;
+        const uint64_t *c1 = ct + ((size_t)L + j) * N;
+        const uint64_t *sh = sk->s_hat.data() + (size_t)j * N;
+        uint64_t *xj = x.data() + (size_t)j * N;
+        for (uint32_t i = 0; i < N; ++i) {
+            const uint64_t v = mulmod(c1[i] % q, sh[i], q);
+            const uint64_t u = c0[i] % q;
+            xj[i] = u + v >= q ? u + v - q : u + v;
+        }
+        c->host_q[j].inverse(xj);
+    }
+    const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nth; ++w)
+        pool.emplace_back([&, w] {
+            for (uint32_t i = w; i < N; i += nth) slots[i] = c->crt.round_coeff(x.data() + i, N);
+        });
+    for (auto &th : pool) th.join();
+    c->host_t.forward(slots);
+}
+
+ephdc_status ephdc_decrypt_slots(const ephdc_ctx *c, const ephdc_sk *sk, const uint64_t *h_ct, uint64_t *h_slots) {
+    if (!c || !sk || !h_ct || !h_slots) return EPHDC_ENULL;
+    if (sk->ctx != c) return EPHDC_ECONTEXT;
+    decrypt_one(c, sk, h_ct, h_slots);
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_decrypt_scores(const ephdc_ctx *c, const ephdc_sk *sk, const uint64_t *h_ct, uint32_t nq,
+                                  int64_t *h_scores, uint32_t *h_labels) {
+    if (!c || !sk || ((!h_ct || !h_scores) && nq)) return EPHDC_ENULL;
+    if (sk->ctx != c) return EPHDC_ECONTEXT;
+    const uint32_t N = c->N, k = c->p.k, B = c->B;
+    const uint32_t nb = (nq + B - 1) / B;
+    const int64_t t = (int64_t)c->t;
+    std::vector<uint64_t> slots(N);
+    for (uint32_t b = 0; b < nb; ++b) {
+        decrypt_one(c, sk, h_ct + (size_t)b * 2 * c->L * N, slots.data());
+        const uint32_t n_b = std::min(B, nq - b * B);
+        for (uint32_t qi = 0; qi < n_b; ++qi) {
+            const uint32_t qg = b * B + qi;
+            int64_t best = 0;
+            uint32_t arg = 0;
+            for (uint32_t cl = 0; cl < k; ++cl) {
+                int64_t v = (int64_t)slots[(size_t)qi * k + cl];
+                if (v > (t - 1) / 2) v -= t;
+                h_scores[(size_t)qg * k + cl] = v;
+                if (cl == 0 || v > best) { best = v; arg = cl; }
+            }
+            if (h_labels) h_labels[qg] = arg;
+        }
+    }
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// standalone kernels (c5)
+// ------------------------------------------------------------------------------------
+void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
+    if (!p) return;
+    if (p->device >= 0) {
+        cudaSetDevice(p->device);
+        cudaFree(p->tw);
+        cudaFree(p->itw);
+        cudaFree(p->ninv);
+    }
+    delete p;
+}
+
+ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device, ephdc_ntt_plan **out) {
+    if (!q || !out) return EPHDC_ENULL;
+    *out = nullptr;
+    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 14) return EPHDC_EPARAM;
+    for (uint32_t j = 0; j < L; ++j)
+        if (q[j] >= (1ull << 61) || !is_ntt_prime(q[j], log2N)) return EPHDC_EPARAM;
+    if (device < 0) return EPHDC_ECONTEXT;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) return EPHDC_ECUDA;
+    EPHDC_CUDA_TRY(cudaSetDevice(device));
+    std::unique_ptr<ephdc_ntt_plan> p(new (std::nothrow) ephdc_ntt_plan());
+    if (!p) return EPHDC_ERESOURCE;
+    p->q.assign(q, q + L);
+    p->L = L;
+    p->log2N = log2N;
+    p->N = 1u << log2N;
+    p->device = device;
+    fill_prime_set(p->ps, p->q, 0);
+    const uint32_t N = p->N;
+    std::vector<TwPair<u64>> tw((size_t)L * N), itw((size_t)L * N);
+    std::vector<uint64_t> ninv(2 * L);
+    for (uint32_t j = 0; j < L; ++j) {
+        const uint64_t psi = min_primitive_root_2n(q[j], log2N);
+        auto f = make_tw64(psi, q[j], log2N);
+        auto g = make_tw64(invmod(psi, q[j]), q[j], log2N);
+        std::copy(f.begin(), f.end(), tw.begin() + (size_t)j * N);
+        std::copy(g.begin(), g.end(), itw.begin() + (size_t)j * N);
+        ninv[2 * j] = invmod(N % q[j], q[j]);
+        ninv[2 * j + 1] = shoup64(ninv[2 * j], q[j]);
+    }
+    if (dev_alloc(&p->tw, tw.size()) != cudaSuccess || dev_alloc(&p->itw, itw.size()) != cudaSuccess ||
+        dev_alloc(&p->ninv, ninv.size()) != cudaSuccess) {
+        ephdc_ntt_plan_free(p.release());
+        return EPHDC_ERESOURCE;
+    }
+    if (cudaMemcpy(p->tw, tw.data(), sizeof(tw[0]) * tw.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->itw, itw.data(), sizeof(itw[0]) * itw.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->ninv, ninv.data(), sizeof(uint64_t) * ninv.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        ephdc_ntt_plan_free(p.release());
+        return EPHDC_ECUDA;
+    }
+    *out = p.release();
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
+    if (!p || (!d_polys && batch)) return EPHDC_ENULL;
+    EPHDC_CUDA_TRY(cudaSetDevice(p->device));
+    EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, false, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
+    if (!p || (!d_polys && batch)) return EPHDC_ENULL;
+    EPHDC_CUDA_TRY(cudaSetDevice(p->device));
+    EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, true, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D, uint64_t *d_out,
+                       void *stream) {
+    if (!p || !d_out || ((!d_ct || !d_pt) && D)) return EPHDC_ENULL;
+    EPHDC_CUDA_TRY(cudaSetDevice(p->device));
+    EPHDC_CUDA_TRY(launch_mac(p, d_ct, d_pt, D, d_out, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// internal.h -- library-internal structures shared by api.cu and kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <vector>
+
+#include "../../include/ephdc.h"
+#include "host_math.h"
+#include "modarith.cuh"
+
+namespace ephdc {
+
+constexpr int kMaxL = EPHDC_MAX_PRIMES;
+
+// Kernel arguments passed by value (fit in the 4 KB parameter space).
+struct PrimeSet {
+    u64 q[kMaxL];
+    u64 qinv[kMaxL];   // q^-1 mod 2^64 (Montgomery)
+    u64 r2[kMaxL];     // 2^128 mod q (undoes the 2^-64 of Montgomery sums)
+    u64 qmt[kMaxL];    // q - t (centered lift, reading #3)
+    u64 delta[kMaxL];  // floor(Q/t) mod q (reading #4)
+    u64 delta_p[kMaxL];// Shoup companion of delta
+    u64 mask[kMaxL];   // 2^ceil(log2 q) - 1 (rejection sampling, reading #8)
+};
+
+struct ctxDev {
+    TwPair<u64> *tw_q = nullptr;   // [L][N] forward twiddles mod q_j
+    TwPair<u32> *itw_t = nullptr;  // [N] inverse twiddles mod t
+    u64 *cdt = nullptr;            // [20]
+};
+
+}  // namespace ephdc
+
+struct ephdc_ctx {
+    ephdc_params p{};
+    std::vector<uint64_t> q;
+    uint32_t N = 0, L = 0, B = 0;
+    uint64_t t = 0, psi_t = 0;
+    std::vector<uint64_t> psi, delta;
+    uint32_t ninv_t = 0, ninv_t_p = 0;
+    ephdc::PrimeSet ps{};
+    uint64_t cdt[20]{};
+    // host NTTs (keygen, decrypt)
+    std::vector<ephdc_host::HostNtt> host_q;
+    ephdc_host::HostNtt host_t;
+    ephdc_host::CrtRound crt;
+    // device
+    int device = -1;
+    ephdc::ctxDev dev;
+    uint32_t fused_S = 1, fused_chunks = 1, fused_G = 1;
+};
+
+struct ephdc_sk {
+    const ephdc_ctx *ctx = nullptr;
+    std::vector<int8_t> s;
+    std::vector<uint64_t> s_hat;  // [L][N]
+};
+
+struct ephdc_model {
+    const ephdc_ctx *ctx = nullptr;
+    uint64_t *d_ct = nullptr;     // [D_live][L][2][N]
+    uint32_t D = 0;
+};
+
+struct ephdc_workspace {
+    const ephdc_ctx *ctx = nullptr;
+    uint32_t max_nq = 0;
+    uint32_t *d_M = nullptr;      // [D_live][N] encoded plaintexts (mod t) of one batch
+    void *d_X = nullptr;          // [max_nq][F]
+    int8_t *d_H = nullptr;        // [D_live][max_nq]
+    uint64_t *d_out = nullptr;    // [nb_max][2][L][N]
+    uint32_t nb_max = 0;
+    // timing
+    bool timing = false;
+    static constexpr int kClasses = 4;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_marks;  // (class, event index of start; end = +1)
+    double ms[kClasses]{};
+    uint64_t launches[kClasses]{};
+    cudaStream_t last_stream = nullptr;
+};
+
+struct ephdc_ntt_plan {
+    std::vector<uint64_t> q;
+    uint32_t L = 0, log2N = 0, N = 0;
+    int device = -1;
+    ephdc::PrimeSet ps{};
+    TwPair<u64> *tw = nullptr, *itw = nullptr;  // [L][N]
+    uint64_t *ninv = nullptr;                            // [L][2] (N^-1, Shoup)
+};
+
+namespace ephdc {
+
+extern std::atomic<uint64_t> g_launches;
+
+// ---- launchers (kernels.cu); all return cudaGetLastError() after the launch ----
+cudaError_t launch_encode(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, void *d_H, bool raw,
+                          cudaStream_t st);
+cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t d0,
+                                     uint32_t nd, uint32_t *d_M, cudaStream_t st);
+cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
+                                   cudaStream_t st);
+cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64_t *d_model, uint64_t *d_out,
+                           cudaStream_t st);
+cudaError_t launch_finalize(const ephdc_ctx *c, uint64_t *d_out, cudaStream_t st);
+cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
+                                 cudaStream_t st);
+cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t d0, uint32_t nd,
+                           const uint64_t *d_shat_mont, uint64_t seed, uint64_t *d_model, cudaStream_t st);
+cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
+                             cudaStream_t st);
+cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
+                       uint64_t *d_out, cudaStream_t st);
+size_t ntt_mac_smem_bytes(uint32_t log2Nc);
+int ntt_mac_occupancy(uint32_t log2N, uint32_t S);
+
+}  // namespace ephdc

@@ -1,0 +1,595 @@
+// kernels.cu -- sm_100a kernels of the EP-HDC client hot path and their launchers.
+//
+//  K1 k_encode        HDC encoding GEMM + quantisation          [int8 dp4a]
+//  K2 k_pack_intt     slot pack + inverse NTT mod t ("EncPt")
+//  K3+K4 k_ntt_mac    centered lift (#3) + forward NTT mod q_j + ct x pt MAC over a
+//                     chunk of dims, atomically folded into the scores
+//  k_finalize         canonical scores ciphertext (undo the Montgomery 2^-64)
+//  k_encrypt          model encryption c0 = NTT(Delta m + e) - a s, c1 = a
+//  k_ntt_batch / k_mac  standalone kernels of the c5 microbench
+// DESIGN.md "Kernels" gives each kernel's roofline and algorithmic bytes/ops.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "ntt_dev.cuh"
+#include "rng.cuh"
+
+namespace ephdc {
+
+std::atomic<uint64_t> g_launches{0};
+
+using namespace ephdc_ntt;
+
+constexpr int kE = 16;  // elements per thread in every NTT pass
+
+// streaming (evict-first) 64-bit load for data read once
+EPHDC_D u64 ldcs64(const u64 *p) { return (u64)__ldcs(reinterpret_cast<const unsigned long long *>(p)); }
+
+// =====================================================================================
+// K1: encoder  acc[d][q] = sum_f P[d][f] X[q][f];  h = clamp((acc + 2^(s-1)) >> s)
+// =====================================================================================
+template <bool UNSIGNED_X>
+__device__ __forceinline__ int dot4(int a, int b, int c) {
+    int r;
+    if constexpr (UNSIGNED_X) asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    else asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+template <bool UNSIGNED_X, bool RAW>
+__global__ void __launch_bounds__(256) k_encode(const uint8_t *__restrict__ X, const int8_t *__restrict__ P, u32 nq,
+                                                u32 F, u32 D_live, u32 shift, int qmax, void *__restrict__ Hout) {
+    constexpr int TD = 64, TQ = 64, KW = 16;  // tile 64 dims x 64 queries, 64-byte K step
+    __shared__ int Ps[TD][KW + 1];
+    __shared__ int Xs[TQ][KW + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const u32 d0 = blockIdx.y * TD, q0 = blockIdx.x * TQ;
+    int acc[4][4] = {};
+    const u32 FW = F >> 2;
+    for (u32 k0 = 0; k0 < FW; k0 += KW) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int idx = threadIdx.x + r * 256;
+            const int row = idx >> 4, w = idx & 15;
+            const u32 kw = k0 + w;
+            int pv = 0, xv = 0;
+            if (kw < FW) {
+                if (d0 + row < D_live) pv = *reinterpret_cast<const int *>(P + (size_t)(d0 + row) * F + 4 * kw);
+                if (q0 + row < nq) xv = *reinterpret_cast<const int *>(X + (size_t)(q0 + row) * F + 4 * kw);
+            }
+            Ps[row][w] = pv;
+            Xs[row][w] = xv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+            int a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = Ps[ty * 4 + i][w];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) b[i] = Xs[tx * 4 + i][w];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) acc[i][jj] = dot4<UNSIGNED_X>(a[i], b[jj], acc[i][jj]);
+        }
+        __syncthreads();
+    }
+    const int rnd = shift ? (1 << (shift - 1)) : 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const u32 d = d0 + ty * 4 + i;
+        if (d >= D_live) continue;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const u32 q = q0 + tx * 4 + jj;
+            if (q >= nq) continue;
+            if constexpr (RAW) {
+                reinterpret_cast<int *>(Hout)[(size_t)d * nq + q] = acc[i][jj];
+            } else {
+                int h = (acc[i][jj] + rnd) >> shift;   // arithmetic shift = floor division
+                h = max(-qmax, min(qmax, h));
+                reinterpret_cast<int8_t *>(Hout)[(size_t)d * nq + q] = (int8_t)h;
+            }
+        }
+    }
+}
+
+// =====================================================================================
+// K2: slot pack + INTT mod t.  One CTA per dim; output M[d][N] (u32, canonical).
+// =====================================================================================
+struct PackArgs {
+    u32 t, two_t, ninv, ninv_p;
+    u32 k, B, D_live;
+    const TwPair<u32> *itw;
+};
+
+template <int LG, bool MODEL>
+__global__ void __launch_bounds__((1 << LG) / kE)
+    k_pack_intt(const int8_t *__restrict__ src, u32 nq, u32 b, u32 d0, PackArgs a, u32 *__restrict__ M) {
+    constexpr int N = 1 << LG, NT = N / kE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    u32 *buf = reinterpret_cast<u32 *>(smem_raw);
+    const u32 d = d0 + blockIdx.x;
+    u32 lim;
+    const int8_t *row;
+    if constexpr (MODEL) {
+        lim = a.k * a.B;                 // model tile: slot i <- C[i mod k][d], i < k*B
+        row = src + d;                   // src = class_hv [k][D_live]
+    } else {
+        const u32 nb = min(a.B, nq - b * a.B);
+        lim = a.k * nb;                  // query slots: slot i <- h[d][b*B + i/k], i < k*n_b
+        row = src + (size_t)d * nq + (size_t)b * a.B;
+    }
+    const u32 k = a.k, t = a.t;
+    auto load = [&](int i) -> u32 {
+        if ((u32)i >= lim) return 0u;
+        int v;
+        if constexpr (MODEL) v = row[(size_t)((u32)i % k) * a.D_live];
+        else v = row[(u32)i / k];
+        return v < 0 ? (u32)((int)t + v) : (u32)v;
+    };
+    inv_ntt<u32, LG, kE>(buf, load, a.itw, t);
+    u32 *out = M + (size_t)blockIdx.x * N;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+        const int pos = threadIdx.x + e * NT;
+        u32 y = mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t);
+        out[pos] = csub(y, t);
+    }
+}
+
+// =====================================================================================
+// K3+K4: centered lift + forward NTT mod q_j + MAC over a chunk of dims.
+// CTA = (prime j, slice s of S, dim chunk); NC = N/S coefficients per CTA.
+// =====================================================================================
+struct MacArgs {
+    PrimeSet ps;
+    u32 t, half_t;       // lift threshold (t-1)/2
+    u32 L, D_live, G;    // G = dims per chunk
+    const TwPair<u64> *tw;  // [L][N]
+};
+
+template <int LGC, int S>
+__global__ void __launch_bounds__((1 << LGC) / kE)
+    k_ntt_mac(const u32 *__restrict__ M, const u64 *__restrict__ model, u64 *__restrict__ out, MacArgs a) {
+    constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    u64 *buf = reinterpret_cast<u64 *>(smem_raw);
+    u64 *acc = buf + padded_len(NC);  // [2][kE][NT], thread-private columns
+    const int tid = threadIdx.x;
+    const u32 x = blockIdx.x;
+    const u32 js = x % (a.L * S), chunk = x / (a.L * S);
+    const u32 j = js / S, s = js % S;
+    const u64 q = a.ps.q[j], qinv = a.ps.qinv[j], two_q = 2 * q, qmt = a.ps.qmt[j];
+    const TwPair<u64> *tw = a.tw + (size_t)j * N;
+    const u32 d0 = chunk * a.G, d1 = min(a.D_live, d0 + a.G);
+#pragma unroll
+    for (int e = 0; e < 2 * kE; ++e) acc[e * NT + tid] = 0;
+    TwPair<u64> w1{0, 0};
+    if constexpr (S > 1) w1 = tw[1];
+    const u32 half_t = a.half_t;
+    for (u32 d = d0; d < d1; ++d) {
+        const u32 *m = M + (size_t)d * N;
+        auto lift = [&](u32 v) -> u64 { return v <= half_t ? (u64)v : (u64)v + qmt; };
+        auto load = [&](int pos) -> u64 {
+            const u64 U = lift(__ldg(m + pos));
+            if constexpr (S == 1) {
+                return U;
+            } else {
+                // first global stage (half-size N/2) fused into the load: slice s keeps U +- w V
+                const u64 V = lift(__ldg(m + pos + NC));
+                const u64 T = mul_shoup_lazy<u64>(V, w1.w, w1.wp, q);
+                return s == 0 ? U + T : U + two_q - T;
+            }
+        };
+        fwd_ntt<u64, LGC, kE>(buf, load, tw, (u32)(N + s * NC), q);
+        const u64 *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
+        const u64 *c1 = c0 + N;
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+            const int pos = tid + e * NT;
+            const u64 p = reduce4<u64>(buf[pad(pos)], q, two_q);
+            const u64 r0 = mont_mul(ldcs64(c0 + pos), p, q, qinv);
+            const u64 r1 = mont_mul(ldcs64(c1 + pos), p, q, qinv);
+            acc[e * NT + tid] = csub(acc[e * NT + tid] + r0, q);
+            acc[(kE + e) * NT + tid] = csub(acc[(kE + e) * NT + tid] + r1, q);
+        }
+        __syncthreads();
+    }
+    u64 *o0 = out + ((size_t)0 * a.L + j) * N + (size_t)s * NC;
+    u64 *o1 = out + ((size_t)1 * a.L + j) * N + (size_t)s * NC;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+        const int pos = tid + e * NT;
+        atomicAdd(reinterpret_cast<unsigned long long *>(o0 + pos), acc[e * NT + tid]);
+        atomicAdd(reinterpret_cast<unsigned long long *>(o1 + pos), acc[(kE + e) * NT + tid]);
+    }
+}
+
+// out[c][j][i] <- (out mod q_j) * 2^64 mod q_j  (undo the 2^-64 of the Montgomery products)
+__global__ void k_finalize(u64 *__restrict__ out, u32 L, u32 N, PrimeSet ps, u32 n_total) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_total) return;
+    const u32 j = (i / N) % L;
+    const u64 q = ps.q[j];
+    out[i] = mont_mul(out[i] % q, ps.r2[j], q, ps.qinv[j]);
+}
+
+// Plaintext NTTs for parity export: p_hat[dd][j] = NTT_j(lift(M[dd])) (full N, one CTA per (dd, j)).
+template <int LG>
+__global__ void __launch_bounds__((1 << LG) / kE)
+    k_plaintext_ntt(const u32 *__restrict__ M, u64 *__restrict__ pt, MacArgs a) {
+    constexpr int N = 1 << LG, NT = N / kE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    u64 *buf = reinterpret_cast<u64 *>(smem_raw);
+    const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L;
+    const u64 q = a.ps.q[j], qmt = a.ps.qmt[j];
+    const u32 *m = M + (size_t)dd * N;
+    const u32 half_t = a.half_t;
+    auto load = [&](int pos) -> u64 {
+        const u32 v = m[pos];
+        return v <= half_t ? (u64)v : (u64)v + qmt;
+    };
+    fwd_ntt<u64, LG, kE>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
+    u64 *o = pt + ((size_t)dd * a.L + j) * N;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+        const int pos = threadIdx.x + e * NT;
+        o[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
+    }
+}
+
+// =====================================================================================
+// Model encryption: per (dim d, prime j): x = [Delta m_d + e_d]_q, c1 = a, c0 = NTT(x) - a s
+// =====================================================================================
+struct EncArgs {
+    PrimeSet ps;
+    u32 L;
+    u64 seed;
+    const u64 *cdt;
+    const u64 *shat_mont;   // [L][N], s_hat * 2^64 mod q
+    const TwPair<u64> *tw;  // [L][N]
+};
+
+template <int LG>
+__global__ void __launch_bounds__((1 << LG) / kE)
+    k_encrypt(const u32 *__restrict__ M, u32 d0, EncArgs a, u64 *__restrict__ model) {
+    constexpr int N = 1 << LG, NT = N / kE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    u64 *buf = reinterpret_cast<u64 *>(smem_raw);
+    __shared__ u64 cdt[ephdc_rng::kCdtLen];
+    if (threadIdx.x < ephdc_rng::kCdtLen) cdt[threadIdx.x] = a.cdt[threadIdx.x];
+    __syncthreads();
+    const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L, d = d0 + dd;
+    const u64 q = a.ps.q[j], delta = a.ps.delta[j], delta_p = a.ps.delta_p[j];
+    const u32 *m = M + (size_t)dd * N;
+    const u64 seed = a.seed;
+    auto load = [&](int pos) -> u64 {
+        const u64 x = mul_shoup_lazy<u64>((u64)m[pos], delta, delta_p, q);  // Delta*m in [0, 2q)
+        const int e = ephdc_rng::gaussian(seed, d, (u32)pos, cdt);
+        return e >= 0 ? x + (u64)e : x + q - (u64)(-e);                     // [0, 4q)
+    };
+    fwd_ntt<u64, LG, kE>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
+    u64 *c0 = model + (((size_t)d * a.L + j) * 2) * N;
+    u64 *c1 = c0 + N;
+    const u64 *sh = a.shat_mont + (size_t)j * N;
+    const u64 mask = a.ps.mask[j];
+#pragma unroll 4
+    for (int e = 0; e < kE; ++e) {
+        const int pos = threadIdx.x + e * NT;
+        const u64 xh = reduce4<u64>(buf[pad(pos)], q, 2 * q);
+        const u64 av = ephdc_rng::uniform_mod(seed, d, j, a.L, (u32)pos, q, mask);
+        const u64 as = mont_mul(av, sh[pos], q, a.ps.qinv[j]);
+        c0[pos] = xh >= as ? xh - as : xh + q - as;
+        c1[pos] = av;
+    }
+}
+
+// =====================================================================================
+// Standalone batched NTT (c5): CTA per (poly, prime), in place on [batch][L][N].
+// =====================================================================================
+struct NttArgs {
+    PrimeSet ps;
+    u32 L;
+    const TwPair<u64> *tw;   // [L][N]
+    const u64 *ninv;         // [L][2]
+};
+
+template <int LG, bool INV>
+__global__ void __launch_bounds__((1 << LG) / kE) k_ntt_batch(u64 *__restrict__ polys, NttArgs a) {
+    constexpr int N = 1 << LG, NT = N / kE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    u64 *buf = reinterpret_cast<u64 *>(smem_raw);
+    const u32 j = blockIdx.x % a.L;
+    u64 *p = polys + (size_t)blockIdx.x * N;
+    const u64 q = a.ps.q[j];
+    const TwPair<u64> *tw = a.tw + (size_t)j * N;
+    auto load = [&](int pos) -> u64 { return p[pos]; };
+    if constexpr (!INV) {
+        fwd_ntt<u64, LG, kE>(buf, load, tw, (u32)N, q);
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+            const int pos = threadIdx.x + e * NT;
+            p[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
+        }
+    } else {
+        inv_ntt<u64, LG, kE>(buf, load, tw, q);
+        const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+            const int pos = threadIdx.x + e * NT;
+            p[pos] = csub(mul_shoup_lazy<u64>(buf[pad(pos)], ni, nip, q), q);
+        }
+    }
+}
+
+// Standalone MAC: each thread owns 2 consecutive coefficients of one prime, loops over a d-range.
+__global__ void __launch_bounds__(256) k_mac(const u64 *__restrict__ ct, const u64 *__restrict__ pt, u32 D, u32 L,
+                                             u32 N, u32 dsplit, PrimeSet ps, u64 *__restrict__ out) {
+    const u32 pairs = (L * N) >> 1;
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= pairs) return;
+    const u32 lin = 2 * g, j = lin / N, i = lin % N;
+    const u64 q = ps.q[j], qinv = ps.qinv[j];
+    const u32 per = (D + dsplit - 1) / dsplit;
+    const u32 d0 = blockIdx.y * per, d1 = min(D, d0 + per);
+    u64 a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+#pragma unroll 4
+    for (u32 d = d0; d < d1; ++d) {
+        const ulonglong2 p = __ldcs(reinterpret_cast<const ulonglong2 *>(pt + ((size_t)d * L + j) * N + i));
+        const ulonglong2 c0 = __ldcs(reinterpret_cast<const ulonglong2 *>(ct + (((size_t)d * L + j) * 2) * N + i));
+        const ulonglong2 c1 = __ldcs(reinterpret_cast<const ulonglong2 *>(ct + (((size_t)d * L + j) * 2 + 1) * N + i));
+        a00 = csub(a00 + mont_mul(c0.x, p.x, q, qinv), q);
+        a01 = csub(a01 + mont_mul(c0.y, p.y, q, qinv), q);
+        a10 = csub(a10 + mont_mul(c1.x, p.x, q, qinv), q);
+        a11 = csub(a11 + mont_mul(c1.y, p.y, q, qinv), q);
+    }
+    unsigned long long *o = reinterpret_cast<unsigned long long *>(out + (size_t)j * 2 * N + i);
+    atomicAdd(o, a00);
+    atomicAdd(o + 1, a01);
+    atomicAdd(o + N, a10);
+    atomicAdd(o + N + 1, a11);
+}
+
+// =====================================================================================
+// launchers
+// =====================================================================================
+template <class K> static cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+static inline cudaError_t counted(cudaError_t e, uint64_t n = 1) {
+    if (e == cudaSuccess) g_launches.fetch_add(n, std::memory_order_relaxed);
+    return e;
+}
+
+cudaError_t launch_encode(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, void *d_H, bool raw,
+                          cudaStream_t st) {
+    dim3 grid((nq + 63) / 64, (c->p.D_live + 63) / 64);
+    const int qmax = (1 << (c->p.Qbits - 1)) - 1;
+    const uint8_t *X = (const uint8_t *)d_X;
+    const u32 F = c->p.F, D = c->p.D_live, s = c->p.qshift;
+    if (c->p.feat_unsigned) {
+        if (raw) k_encode<true, true><<<grid, 256, 0, st>>>(X, d_P, nq, F, D, s, qmax, d_H);
+        else k_encode<true, false><<<grid, 256, 0, st>>>(X, d_P, nq, F, D, s, qmax, d_H);
+    } else {
+        if (raw) k_encode<false, true><<<grid, 256, 0, st>>>(X, d_P, nq, F, D, s, qmax, d_H);
+        else k_encode<false, false><<<grid, 256, 0, st>>>(X, d_P, nq, F, D, s, qmax, d_H);
+    }
+    return counted(cudaGetLastError());
+}
+
+static PackArgs pack_args(const ephdc_ctx *c) {
+    PackArgs a;
+    a.t = (u32)c->t;
+    a.two_t = (u32)(2 * c->t);
+    a.ninv = c->ninv_t;
+    a.ninv_p = c->ninv_t_p;
+    a.k = c->p.k;
+    a.B = c->B;
+    a.D_live = c->p.D_live;
+    a.itw = c->dev.itw_t;
+    return a;
+}
+
+template <int LG, bool MODEL>
+static cudaError_t pack_launch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 d0, u32 nd, u32 *M,
+                               cudaStream_t st) {
+    const size_t smem = sizeof(u32) * padded_len(1 << LG);
+    auto kern = k_pack_intt<LG, MODEL>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<nd, (1 << LG) / kE, smem, st>>>(src, nq, b, d0, pack_args(c), M);
+    return counted(cudaGetLastError());
+}
+
+template <bool MODEL>
+static cudaError_t pack_dispatch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 d0, u32 nd, u32 *M,
+                                 cudaStream_t st) {
+    if (nd == 0) return cudaSuccess;
+    switch (c->p.log2N) {
+        case 10: return pack_launch<10, MODEL>(c, src, nq, b, d0, nd, M, st);
+        case 11: return pack_launch<11, MODEL>(c, src, nq, b, d0, nd, M, st);
+        case 12: return pack_launch<12, MODEL>(c, src, nq, b, d0, nd, M, st);
+        case 13: return pack_launch<13, MODEL>(c, src, nq, b, d0, nd, M, st);
+        case 14: return pack_launch<14, MODEL>(c, src, nq, b, d0, nd, M, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t d0,
+                                     uint32_t nd, uint32_t *d_M, cudaStream_t st) {
+    return pack_dispatch<false>(c, d_H, nq, b, d0, nd, d_M, st);
+}
+
+cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
+                                   cudaStream_t st) {
+    return pack_dispatch<true>(c, d_C, 0, 0, d0, nd, d_M, st);
+}
+
+static MacArgs mac_args(const ephdc_ctx *c) {
+    MacArgs a;
+    a.ps = c->ps;
+    a.t = (u32)c->t;
+    a.half_t = (u32)((c->t - 1) / 2);
+    a.L = c->L;
+    a.D_live = c->p.D_live;
+    a.G = c->fused_G;
+    a.tw = c->dev.tw_q;
+    return a;
+}
+
+size_t ntt_mac_smem_bytes(uint32_t lgc) {
+    const size_t nc = (size_t)1 << lgc;
+    return sizeof(u64) * (padded_len((int)nc) + 2 * nc);
+}
+
+template <int LGC, int S>
+static cudaError_t ntt_mac_launch(const ephdc_ctx *c, const u32 *M, const u64 *model, u64 *out, cudaStream_t st) {
+    const size_t smem = ntt_mac_smem_bytes(LGC);
+    auto kern = k_ntt_mac<LGC, S>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const u32 grid = c->L * S * c->fused_chunks;
+    kern<<<grid, (1 << LGC) / kE, smem, st>>>(M, model, out, mac_args(c));
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64_t *d_model, uint64_t *d_out,
+                           cudaStream_t st) {
+    switch (c->p.log2N) {
+        case 10: return ntt_mac_launch<10, 1>(c, d_M, d_model, d_out, st);
+        case 11: return ntt_mac_launch<11, 1>(c, d_M, d_model, d_out, st);
+        case 12: return ntt_mac_launch<12, 1>(c, d_M, d_model, d_out, st);
+        case 13: return ntt_mac_launch<13, 1>(c, d_M, d_model, d_out, st);
+        case 14: return ntt_mac_launch<13, 2>(c, d_M, d_model, d_out, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int ntt_mac_occupancy(uint32_t log2N, uint32_t S) {
+    const uint32_t lgc = log2N - (S == 2 ? 1 : 0);
+    const size_t smem = ntt_mac_smem_bytes(lgc);
+    int per_sm = (int)((227 * 1024) / smem);
+    return per_sm < 1 ? 1 : per_sm;
+}
+
+cudaError_t launch_finalize(const ephdc_ctx *c, uint64_t *d_out, cudaStream_t st) {
+    const u32 n = 2 * c->L * c->N;
+    k_finalize<<<(n + 255) / 256, 256, 0, st>>>(d_out, c->L, c->N, c->ps, n);
+    return counted(cudaGetLastError());
+}
+
+template <int LG>
+static cudaError_t pt_launch(const ephdc_ctx *c, const u32 *M, u32 nd, u64 *pt, cudaStream_t st) {
+    const size_t smem = sizeof(u64) * padded_len(1 << LG);
+    auto kern = k_plaintext_ntt<LG>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<nd * c->L, (1 << LG) / kE, smem, st>>>(M, pt, mac_args(c));
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
+                                 cudaStream_t st) {
+    if (nd == 0) return cudaSuccess;
+    switch (c->p.log2N) {
+        case 10: return pt_launch<10>(c, d_M, nd, d_pt, st);
+        case 11: return pt_launch<11>(c, d_M, nd, d_pt, st);
+        case 12: return pt_launch<12>(c, d_M, nd, d_pt, st);
+        case 13: return pt_launch<13>(c, d_M, nd, d_pt, st);
+        case 14: return pt_launch<14>(c, d_M, nd, d_pt, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int LG>
+static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u32 d0, u32 nd, const u64 *shat, u64 seed, u64 *model,
+                              cudaStream_t st) {
+    const size_t smem = sizeof(u64) * padded_len(1 << LG);
+    auto kern = k_encrypt<LG>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    EncArgs a;
+    a.ps = c->ps;
+    a.L = c->L;
+    a.seed = seed;
+    a.cdt = c->dev.cdt;
+    a.shat_mont = shat;
+    a.tw = c->dev.tw_q;
+    kern<<<nd * c->L, (1 << LG) / kE, smem, st>>>(M, d0, a, model);
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t d0, uint32_t nd,
+                           const uint64_t *d_shat_mont, uint64_t seed, uint64_t *d_model, cudaStream_t st) {
+    if (nd == 0) return cudaSuccess;
+    switch (c->p.log2N) {
+        case 10: return enc_launch<10>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
+        case 11: return enc_launch<11>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
+        case 12: return enc_launch<12>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
+        case 13: return enc_launch<13>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
+        case 14: return enc_launch<14>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int LG, bool INV>
+static cudaError_t nttb_launch(const ephdc_ntt_plan *p, u64 *polys, u32 batch, cudaStream_t st) {
+    const size_t smem = sizeof(u64) * padded_len(1 << LG);
+    auto kern = k_ntt_batch<LG, INV>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    NttArgs a;
+    a.ps = p->ps;
+    a.L = p->L;
+    a.tw = INV ? p->itw : p->tw;
+    a.ninv = p->ninv;
+    // grid.x limit is 2^31-1: batch * L fits
+    kern<<<batch * p->L, (1 << LG) / kE, smem, st>>>(polys, a);
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
+                             cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+#define EPHDC_NTTB(LG) \
+    case LG: return inverse ? nttb_launch<LG, true>(p, d_polys, batch, st) : nttb_launch<LG, false>(p, d_polys, batch, st);
+    switch (p->log2N) {
+        EPHDC_NTTB(10)
+        EPHDC_NTTB(11)
+        EPHDC_NTTB(12)
+        EPHDC_NTTB(13)
+        EPHDC_NTTB(14)
+    }
+#undef EPHDC_NTTB
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
+                       uint64_t *d_out, cudaStream_t st) {
+    const u32 L = p->L, N = p->N;
+    cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(u64) * 2 * L * N, st);
+    if (e != cudaSuccess) return e;
+    if (D == 0) return cudaSuccess;
+    const u32 pairs = (L * N) / 2;
+    const u32 bx = (pairs + 255) / 256;
+    u64 qmax = 0;
+    for (u32 j = 0; j < L; ++j) qmax = std::max<u64>(qmax, p->q[j]);
+    u32 max_split = (u32)std::min<u64>(~0ull / qmax, 1u << 16);
+    u32 dsplit = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
+    dsplit = std::min(std::min(dsplit, D), max_split);
+    k_mac<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, d_out);
+    e = counted(cudaGetLastError());
+    if (e != cudaSuccess) return e;
+    // finalize: output layout [L][2][N]
+    const u32 n = 2 * L * N;
+    // reuse k_finalize with the [j][c][i] layout: prime index = i / (2N)
+    k_finalize<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
+    return counted(cudaGetLastError());
+}
+
+}  // namespace ephdc

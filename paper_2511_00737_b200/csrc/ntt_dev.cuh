@@ -1,0 +1,132 @@
+// ntt_dev.cuh -- CTA-resident negacyclic NTT passes in shared memory (sm_100a).
+//
+// A CTA of NT = NC/E threads transforms NC = 2^LG residues held in shared memory.
+// Each pass runs up to 4 butterfly stages (radix 16) in registers: a thread loads
+// E = 16 elements (E/R groups of R = 2^r elements at stride tl), applies r stages,
+// and writes them back; one __syncthreads() per pass.  Shared memory is padded by
+// one word per 16 (pad(i) = i + i/16) so that every pass pattern, including the
+// 16-consecutive-element groups of the last forward / first inverse pass, is free
+// of bank conflicts.
+//
+// Index conventions follow the textbook loops (oracle/oracle_core.c is the
+// independent reference):
+//   forward (Cooley-Tukey), stage half-size t, block i: W = psi_rev[N/(2t) + i]
+//   inverse (Gentleman-Sande), stage half-size t, block i: W = psiinv_rev[N/(2t) + i]
+// with psi_rev[k] = psi^brev(k).  A CTA may own one of S = N/NC output slices of a
+// forward NTT (the split used by the fused MAC kernel at N = 16384): the caller then
+// performs the first global stage while loading and passes tw_num = N + s*NC so the
+// block indices are global.
+#pragma once
+#include "modarith.cuh"
+
+namespace ephdc_ntt {
+
+EPHDC_D int pad(int i) { return i + (i >> 4); }
+constexpr int padded_len(int n) { return n + n / 16; }
+
+// One forward pass: local stages with half-sizes 2^T0_LOG ... 2^(T0_LOG-R_LOG+1).
+template <typename W, int LG, int E, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+EPHDC_D void fwd_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ tw, u32 tw_num, W q, W two_q) {
+    constexpr int R = 1 << R_LOG;
+    constexpr int TL_LOG = T0_LOG - (R_LOG - 1);
+    constexpr int TL = 1 << TL_LOG;
+    constexpr int NT = (1 << LG) / E;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+        const int g = tid + u * NT;
+        const int blk = g >> TL_LOG, off = g & (TL - 1);
+        const int base = (blk << (T0_LOG + 1)) + off;
+        W x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
+            else x[k] = buf[pad(base + k * TL)];
+        }
+        const u32 idx0 = (tw_num >> (T0_LOG + 1)) + (u32)blk;
+#pragma unroll
+        for (int sub = 0; sub < R_LOG; ++sub) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int h = R >> (sub + 1);
+#pragma unroll
+            for (int v = 0; v < (1 << sub); ++v) {
+                const TwPair<W> w = tw[(idx0 << sub) + v];
+#pragma unroll
+                for (int kk = 0; kk < h; ++kk) ct_bfly<W>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w, q, two_q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[pad(base + k * TL)] = x[k];
+    }
+    __syncthreads();
+}
+
+template <typename W, int LG, int E, int REM, bool FIRST, class Load>
+EPHDC_D void fwd_passes(W *buf, const Load &load, const TwPair<W> *__restrict__ tw, u32 tw_num, W q, W two_q) {
+    if constexpr (REM > 0) {
+        constexpr int R_LOG = REM >= 4 ? 4 : REM;
+        fwd_pass<W, LG, E, REM - 1, R_LOG, FIRST>(buf, load, tw, tw_num, q, two_q);
+        fwd_passes<W, LG, E, REM - R_LOG, false>(buf, load, tw, tw_num, q, two_q);
+    }
+}
+
+// Forward NTT of NC = 2^LG values produced by load(local_index) (in [0, 4q));
+// result (lazy, [0, 4q)) in buf[pad(i)], bit-reversed evaluation order.
+template <typename W, int LG, int E, class Load>
+EPHDC_D void fwd_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ tw, u32 tw_num, W q) {
+    fwd_passes<W, LG, E, LG, true>(buf, load, tw, tw_num, q, (W)(2 * q));
+}
+
+// One inverse pass: stages with half-sizes 2^T0_LOG ... 2^(T0_LOG+R_LOG-1).
+template <typename W, int LG, int E, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q, W two_q) {
+    constexpr int R = 1 << R_LOG;
+    constexpr int T0 = 1 << T0_LOG;
+    constexpr int NT = (1 << LG) / E;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+        const int g = tid + u * NT;
+        const int blk = g >> T0_LOG, off = g & (T0 - 1);
+        const int base = blk * (T0 * R) + off;
+        W x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            if constexpr (FROM_LOAD) x[k] = load(base + k * T0);
+            else x[k] = buf[pad(base + k * T0)];
+        }
+#pragma unroll
+        for (int sub = 0; sub < R_LOG; ++sub) {
+            const int hs = 1 << sub;
+#pragma unroll
+            for (int v = 0; v < R / (2 * hs); ++v) {
+                const u32 idx = ((u32)(1 << LG) >> (T0_LOG + sub + 1)) + (u32)((blk * R) >> (sub + 1)) + v;
+                const TwPair<W> w = itw[idx];
+#pragma unroll
+                for (int kk = 0; kk < hs; ++kk) gs_bfly<W>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
+    }
+    __syncthreads();
+}
+
+template <typename W, int LG, int E, int DONE, bool FIRST, class Load>
+EPHDC_D void inv_passes(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q, W two_q) {
+    if constexpr (DONE < LG) {
+        constexpr int R_LOG = (LG - DONE) >= 4 ? 4 : (LG - DONE);
+        inv_pass<W, LG, E, DONE, R_LOG, FIRST>(buf, load, itw, q, two_q);
+        inv_passes<W, LG, E, DONE + R_LOG, false>(buf, load, itw, q, two_q);
+    }
+}
+
+// Inverse NTT (without the final N^-1) of values from load(i) in [0, 2q);
+// result (lazy, [0, 2q)) in buf[pad(i)], natural coefficient order.
+template <typename W, int LG, int E, class Load>
+EPHDC_D void inv_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q) {
+    inv_passes<W, LG, E, 0, true>(buf, load, itw, q, (W)(2 * q));
+}
+
+}  // namespace ephdc_ntt

@@ -110,8 +110,8 @@ def test_gaussian_cdt_pins():
     Z = rho[0] + 2 * sum(rho[1:])
     for k in range(19):
         cdf = (rho[0] + 2 * sum(rho[1:k + 1])) / Z
-        assert abs(int(T[k]) / 2.0 ** 63 - cdf) < 2 ** -47
-    # rounding margin: no entry sits near a rounding boundary of the 2^48 grid,
+        assert abs(int(T[k]) / 2.0 ** 63 - cdf) < 2 ** -39
+    # rounding margin: no entry sits near a rounding boundary of the 2^40 grid,
     # so any correct independent evaluation rounds identically
     from decimal import Decimal, getcontext
     getcontext().prec = 50
@@ -119,9 +119,9 @@ def test_gaussian_cdt_pins():
     rd = [(-(Decimal(k) ** 2) / (2 * s * s)).exp() for k in range(20)]
     Zd = rd[0] + 2 * sum(rd[1:])
     for k in range(19):
-        v = (rd[0] + 2 * sum(rd[1:k + 1])) / Zd * (Decimal(2) ** 48)
+        v = (rd[0] + 2 * sum(rd[1:k + 1])) / Zd * (Decimal(2) ** 40)
         frac = v - int(v)
-        assert abs(frac - Decimal("0.5")) > Decimal("1e-6")
+        assert abs(frac - Decimal("0.5")) > Decimal("0.01")
 
 
 def test_sampler_statistics():
