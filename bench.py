@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""EP-HDC client-side encrypted inference on B200: queries/s (BASELINE.json metric).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+A step = the whole hot path over one batch of nq synthetic queries with inputs and
+the encrypted model resident in HBM: ephdc_encode_queries (HDC encoding + Q-bit
+quantisation) + ephdc_infer_batch (per ciphertext batch: slot pack + INTT_t, lift +
+NTT_q + ct x pt MAC over all D dims, finalize) -> nb scores ciphertexts.
+Default workload: c4 (BASELINE.json configs[3], the largest single-GPU config; the
+metric names no config).  Multi-GPU: one process per GPU, each rank a full replica
+on its own nq queries (batches are independent: weak scaling, no data-path
+collective); value = all ranks' queries / max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ephdc_inputs as inp  # noqa: E402
+
+METRIC = "encrypted-HDC queries/sec on 1 B200; NTT+MAC fraction of HBM/int roofline"
+# Integer-pipe peak: 148 SMs x 64 IMAD lanes/clk (fma pipe,
+# rt_SMSP = 2, B300_MICROARCH.md) x max SM clock, / 10 multiply instructions per u64
+# Shoup/Montgomery modular multiply on the 32-bit multiplier.
+IMAD_PER_SM_CLK = 64
+IMAD_PER_MULMOD = 10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=["c1q3", "c2", "c3", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- oracle
+def oracle_sample(cfg, data, budget_s: float):
+    """Oracle (plain CPU, OpenMP over dims) on a bounded sample of the workload:
+    encode + client evaluation of ONE full ciphertext batch (B queries) over the first
+    Ds dims with a stored model; queries/s extrapolated to all D_live dims."""
+    from oracle import pipeline as opipe
+    Xtr, ytr, Xq, P = data
+    om = opipe.build_model(cfg, P, Xtr, ytr)
+    bfv = om.bfv
+    B = bfv.B
+    Xb = Xq[:B]
+    cores = os.cpu_count() or 1
+
+    def run(Ds):
+        C = np.ascontiguousarray(om.class_hv[:, :Ds])
+        bfv.D_live = Ds
+        model = bfv.encrypt_dims(C, om.enc_seed, 0, Ds)            # untimed: model is resident
+        t0 = time.perf_counter()
+        Pd = P[:Ds]
+        from oracle import hdc
+        H = hdc.quantise_queries(hdc.encode_raw(Pd, Xb, Ds), om.qshift, om.Qbits)
+        bfv.infer_batch(H, H.shape[1], 0, model=model)
+        dt = time.perf_counter() - t0
+        bfv.D_live = cfg.D_live
+        return dt
+
+    Ds = max(1, min(cfg.D_live, 2 * cores))
+    dt = run(Ds)
+    if dt < budget_s / 3:
+        Ds = int(min(cfg.D_live, max(Ds + 1, Ds * budget_s / max(dt, 1e-3))))
+        dt = run(Ds)
+    per_batch = dt * cfg.D_live / Ds
+    qps = B / per_batch
+    return {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cfg.name}: encode + evaluation of one full batch ({B} queries) over {Ds} of "
+                      f"{cfg.D_live} dims with a stored model, {dt:.1f} s, extrapolated linearly in D"}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = inp.CONFIGS[a.config]
+
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        Xtr, ytr, Xq, _ = inp.gen_features(cfg)
+        P = inp.gen_projection(cfg)
+        vals = []
+        cb = None
+        for _ in range(a.warmup + a.steps):
+            cb = oracle_sample(cfg, (Xtr, ytr, Xq, P), a.cpu_budget / max(1, a.steps))
+            vals.append(cb["value"])
+        v = statistics.median(vals[a.warmup:])
+        cb["value"] = v
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": a.gpus,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": cfg.nq / v * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "config": {"workload": cfg.name, "nq": cfg.nq, "N": cfg.N, "L": cfg.L, "D": cfg.D_live, "k": cfg.k},
+                "cpu_baseline": cb,
+                "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    import paper_2511_00737_b200 as eph
+    from paper_2511_00737_b200 import pipeline as ppipe
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    Xtr, ytr, Xq, _ = inp.gen_features(cfg)
+    P = inp.gen_projection(cfg)
+    ps = ppipe.build(cfg, P, Xtr, ytr, device=local)
+    ctx, model = ps.ctx, ps.model
+    nq = cfg.nq
+    nb = ctx.n_batches(nq)
+    X_dev = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).to(dev)
+    ws = eph.Workspace(ctx, nq)
+    H = torch.empty((cfg.D_live, nq), dtype=torch.int8, device=dev)
+    out = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eph.encode_queries(ctx, X_dev, ps.P_dev, H)
+        eph.infer_batch(ctx, model, ws, H, nq, out)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ws.set_timing(True)
+    ws.timing()                                  # reset
+    n0 = eph.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = eph.launch_count() - n0
+    kt = ws.timing()
+    ws.set_timing(False)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * nq / (ms_max / 1e3)
+
+    # roofline of the dominant kernel: the fused lift + NTT_q + MAC (one launch per batch)
+    mac_ms, mac_n = kt["ntt_mac"]
+    per_launch_s = mac_ms / max(1, mac_n) / 1e3
+    N, L, D = ctx.N, ctx.L, cfg.D_live
+    mulmods = D * L * ((N // 2) * cfg.log2N + 2 * N)      # butterflies + 2 MAC products per coefficient
+    achieved = mulmods / per_launch_s / 1e9
+    smax = measured_peaks().get("sm_max_mhz") or 1965.0
+    peak = 148 * IMAD_PER_SM_CLK * smax * 1e6 / IMAD_PER_MULMOD / 1e9
+    total_ms = sum(v[0] for v in kt.values())
+    roofline = {"bound": "alu", "kernel": "k_ntt_mac", "achieved": round(achieved, 1), "peak": round(peak, 1),
+                "unit": "Gmulmod/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": "derived: 148 SMs x 64 IMAD/clk x sm_max_mhz / 10 IMAD per u64 mulmod (DESIGN.md)",
+                "share_of_step": round(mac_ms / max(total_ms, 1e-9), 4),
+                "kernel_ms": {k: round(v[0] / a.steps, 3) for k, v in kt.items()}}
+
+    # e2e: the same step through the host-buffer C-ABI call (H2D + compute + D2H per step)
+    e2e = None
+    if not a.no_e2e:
+        Xh = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).pin_memory()
+        oh = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, pin_memory=True)
+        for _ in range(max(1, a.warmup)):
+            eph.classify_host(ctx, model, ws, Xh, ps.P_dev, oh)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.steps):
+            eph.classify_host(ctx, model, ws, Xh, ps.P_dev, oh)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = torch.tensor([f0.elapsed_time(f1) / a.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * nq / (float(ems.item()) / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(Xh.numel()), "d2h_bytes_per_step": int(oh.numel() * 8)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = oracle_sample(cfg, (Xtr, ytr, Xq, P), a.cpu_budget)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": cfg.name, "nq_per_gpu": nq, "batches": nb, "N": N, "L": L, "D": D,
+                           "k": cfg.k, "F": cfg.F, "t": ctx.t, "log2q": sum(int(q).bit_length() for q in ctx.q),
+                           "parallelism": f"replica x{world} (independent query batches)",
+                           "l2": "inputs larger than L2 (encrypted model %.1f GB streamed per batch)"
+                                 % (D * L * 2 * N * 8 / 1e9)},
+                "gpu_launches": int(launches), "clocks": clk, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,58 @@
+"""Standalone kernels of the c5 microbench (BASELINE.json configs[4]) vs the oracle (-m gpu):
+forward / inverse negacyclic NTT and the pointwise ct x pt MAC on uniform residues."""
+import numpy as np
+import pytest
+
+import ephdc_inputs as inp
+from oracle import core, nt
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2511_00737_b200 as eph  # noqa: E402
+
+
+def _dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("log2N", [10, 12, 13, 14])
+@pytest.mark.parametrize("L,bits", [(1, 30), (3, 60), (5, 60), (9, 48), (16, 30), (16, 60)])
+def test_ntt_fwd_inv_bitexact(log2N, L, bits):
+    q = nt.prime_chain([bits] * L, log2N)
+    batch = 3
+    x = inp.gen_residues(q, batch, 1 << log2N, seed=log2N * 100 + L)
+    plan = eph.NttPlan(q, log2N)
+    d = _dev(x)
+    eph.ntt_fwd(plan, d)
+    got = _host(d)
+    for j, p in enumerate(q):
+        psi = nt.min_primitive_2n_root(p, 1 << log2N)
+        want = core.ntt_fwd(x[:, j, :], log2N, p, psi)
+        assert np.array_equal(got[:, j, :], want), (j, p)
+    eph.ntt_inv(plan, d)
+    assert np.array_equal(_host(d), x)
+
+
+@pytest.mark.parametrize("log2N,L,bits,D", [(12, 3, 60, 5), (13, 5, 44, 64), (14, 9, 48, 33), (12, 16, 60, 300)])
+def test_mac_bitexact(log2N, L, bits, D):
+    N = 1 << log2N
+    q = nt.prime_chain([bits] * L, log2N)
+    ct = inp.gen_residues(q * 2, D, N, seed=7)                 # [D][2L][N] -> view as [D][L][2][N]
+    ct = np.stack([ct[:, 2 * j: 2 * j + 2, :] for j in range(L)], axis=1) % np.array(q, dtype=np.uint64)[None, :, None, None]
+    pt = inp.gen_residues(q, D, N, seed=8)
+    plan = eph.NttPlan(q, log2N)
+    out = _host(eph.mac(plan, _dev(ct), _dev(pt)))
+    for j, p in enumerate(q):
+        for c in range(2):
+            acc = np.zeros(N, dtype=object)
+            for d in range(D):
+                acc = (acc + ct[d, j, c].astype(object) * pt[d, j].astype(object)) % p
+            assert np.array_equal(out[j, c], acc.astype(np.uint64)), (j, c)

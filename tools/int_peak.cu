@@ -1,0 +1,86 @@
+// int_peak.cu -- measured integer-pipe throughput on the B200 (denominator of the "alu" roofline).
+// Each kernel runs 8 independent dependency chains per thread of one PTX op; the SASS op
+// it lowers to is checked with cuobjdump. Reports ops/clk/SM using clock64/globaltimer.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o int_peak int_peak.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+constexpr int ITERS = 4096;
+constexpr int CH = 8;
+
+#define KERNEL(NAME, T, INIT, BODY)                                                        \
+    __global__ void NAME(T *out, unsigned long long *clk) {                               \
+        T r[CH];                                                                           \
+        for (int c = 0; c < CH; ++c) r[c] = (T)(threadIdx.x * 7 + c * 13 + INIT);          \
+        const T m = (T)(blockIdx.x | 0x9e3779b9u);                                         \
+        unsigned long long c0 = clock64(), g0;                                             \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));                             \
+        for (int i = 0; i < ITERS; ++i) {                                                  \
+            _Pragma("unroll") for (int c = 0; c < CH; ++c) { BODY; }                       \
+        }                                                                                  \
+        unsigned long long c1 = clock64(), g1;                                             \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));                             \
+        T s = 0;                                                                           \
+        for (int c = 0; c < CH; ++c) s += r[c];                                            \
+        out[blockIdx.x * blockDim.x + threadIdx.x] = s;                                    \
+        if (threadIdx.x == 0 && blockIdx.x == 0) { clk[0] = c1 - c0; clk[1] = g1 - g0; }   \
+    }
+
+// IMAD (32-bit multiply-add, lo)
+KERNEL(k_imad, uint32_t, 1, asm volatile("mad.lo.u32 %0, %0, %1, %0;" : "+r"(r[c]) : "r"(m)))
+// IMAD.HI (32x32 -> high 32)
+KERNEL(k_imadhi, uint32_t, 1, asm volatile("mad.hi.u32 %0, %0, %1, %0;" : "+r"(r[c]) : "r"(m)))
+// IMAD.WIDE (32x32 -> 64 + 64)
+KERNEL(k_imadwide, uint64_t, 1,
+       asm volatile("{ .reg .u32 lo; cvt.u32.u64 lo, %0; mad.wide.u32 %0, lo, %1, %0; }" : "+l"(r[c]) : "r"((uint32_t)m)))
+// IADD3 (alu pipe)
+KERNEL(k_iadd3, uint32_t, 1, asm volatile("add.u32 %0, %0, %1;" : "+r"(r[c]) : "r"(m)))
+// u64 multiply high (emulated: several IMAD-class ops)
+KERNEL(k_mul64hi, uint64_t, 3, asm volatile("mul.hi.u64 %0, %0, %1;" : "+l"(r[c]) : "l"((uint64_t)m * 0x9E3779B97F4A7C15ull)))
+// u64 multiply low
+KERNEL(k_mul64lo, uint64_t, 3, asm volatile("mul.lo.u64 %0, %0, %1;" : "+l"(r[c]) : "l"((uint64_t)m * 0x9E3779B97F4A7C15ull | 1)))
+// FP64 FMA (for reference: the DFMA pipe)
+KERNEL(k_dfma, double, 1, asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(r[c]) : "d"(1.0000001)))
+
+template <class K, class T>
+static void run(const char *name, K kern, int blocks, int threads) {
+    T *out;
+    unsigned long long *clk, h[2];
+    cudaMalloc(&out, sizeof(T) * blocks * threads);
+    cudaMalloc(&clk, 16);
+    kern<<<blocks, threads>>>(out, clk);  // warm-up
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    kern<<<blocks, threads>>>(out, clk);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaMemcpy(h, clk, 16, cudaMemcpyDeviceToHost);
+    const double ops = (double)blocks * threads * ITERS * CH;
+    const double mhz = (double)h[0] / (double)h[1] * 1e3;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const double per_sm_clk = ops / (ms * 1e-3) / sms / (mhz * 1e6);
+    printf("{\"op\": \"%s\", \"Gops\": %.1f, \"per_sm_per_clk\": %.2f, \"sm_mhz\": %.0f, \"ms\": %.3f}\n", name,
+           ops / (ms * 1e-3) / 1e9, per_sm_clk, mhz, ms);
+    cudaFree(out);
+    cudaFree(clk);
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * 8, threads = 256;
+    run<decltype(k_imad), uint32_t>("IMAD(mad.lo.u32)", k_imad, blocks, threads);
+    run<decltype(k_imadhi), uint32_t>("IMAD.HI(mad.hi.u32)", k_imadhi, blocks, threads);
+    run<decltype(k_imadwide), uint64_t>("IMAD.WIDE(mad.wide.u32)", k_imadwide, blocks, threads);
+    run<decltype(k_iadd3), uint32_t>("IADD3(add.u32)", k_iadd3, blocks, threads);
+    run<decltype(k_mul64hi), uint64_t>("mul.hi.u64", k_mul64hi, blocks, threads);
+    run<decltype(k_mul64lo), uint64_t>("mul.lo.u64", k_mul64lo, blocks, threads);
+    run<decltype(k_dfma), double>("DFMA(fma.rn.f64)", k_dfma, blocks, threads);
+    return 0;
+}
