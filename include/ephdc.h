@@ -70,7 +70,18 @@ typedef struct {
     uint32_t Cbits;          /* class HV width, 2..8                              */
     uint32_t qshift;         /* query rounding shift s (reading #13)              */
     double sigma_e;          /* BFV error std-dev (3.2, BASELINE.json configs[0]) */
+    uint32_t arith;          /* modular-arithmetic pipe of the fused NTT+MAC kernel:
+                              * EPHDC_ARITH_AUTO (0): FP64 pipe when every q_j < 2^50
+                              * and the value bounds of DESIGN.md "FP64 modular
+                              * arithmetic" hold, else the integer pipe;
+                              * EPHDC_ARITH_INT (1): integer pipe (u64 Shoup/Montgomery);
+                              * EPHDC_ARITH_F64 (2): FP64 pipe, EPARAM if not eligible.
+                              * Both give bit-identical results.                    */
 } ephdc_params;
+
+#define EPHDC_ARITH_AUTO 0u
+#define EPHDC_ARITH_INT 1u
+#define EPHDC_ARITH_F64 2u
 
 /* Derived values of a context (for tests and tooling). */
 typedef struct {
@@ -82,6 +93,8 @@ typedef struct {
     uint32_t fused_split;    /* S: CTAs per polynomial in the fused MAC kernel   */
     uint32_t fused_chunks;   /* dim chunks per batch in the fused MAC kernel     */
     int device;              /* CUDA device, -1 for a host-only context          */
+    uint32_t arith;          /* selected pipe: EPHDC_ARITH_INT or EPHDC_ARITH_F64 */
+    uint32_t f64_red_every;  /* FP64 path: accumulator reduction interval (dims) */
 } ephdc_ctx_info;
 
 typedef struct ephdc_ctx ephdc_ctx;

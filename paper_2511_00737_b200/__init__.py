@@ -73,10 +73,10 @@ class Context:
 
     def __init__(self, *, log2N: int, q: Sequence[int], t: int, k: int, D_live: int, D_stored: int, F: int,
                  feat_unsigned: bool, Qbits: int, Cbits: int, qshift: int, sigma_e: float = 3.2,
-                 device: int = 0):
+                 device: int = 0, arith: int = 0):
         self._q = np.ascontiguousarray(np.array(q, dtype=np.uint64))
         self.params = _capi.Params(log2N, len(q), self._q.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), t, k,
-                                   D_live, D_stored, F, int(feat_unsigned), Qbits, Cbits, qshift, sigma_e)
+                                   D_live, D_stored, F, int(feat_unsigned), Qbits, Cbits, qshift, sigma_e, arith)
         self._h = ctypes.c_void_p()
         call("ephdc_ctx_create", ctypes.byref(self.params), device, ctypes.byref(self._h))
         info = _capi.CtxInfo()
@@ -91,6 +91,7 @@ class Context:
         self.feat_unsigned = bool(feat_unsigned)
         self.Qbits, self.Cbits, self.qshift = Qbits, Cbits, qshift
         self.device = device
+        self.arith = "f64" if info.arith == _capi.ARITH_F64 else "int"
 
     @property
     def handle(self):

@@ -32,8 +32,11 @@ class Params(ctypes.Structure):
         ("log2N", c_u32), ("L", c_u32), ("q", ctypes.POINTER(c_u64)), ("t", c_u64),
         ("k", c_u32), ("D_live", c_u32), ("D_stored", c_u32), ("F", c_u32),
         ("feat_unsigned", c_u32), ("Qbits", c_u32), ("Cbits", c_u32), ("qshift", c_u32),
-        ("sigma_e", ctypes.c_double),
+        ("sigma_e", ctypes.c_double), ("arith", c_u32),
     ]
+
+
+ARITH_AUTO, ARITH_INT, ARITH_F64 = 0, 1, 2
 
 
 class CtxInfo(ctypes.Structure):
@@ -42,6 +45,7 @@ class CtxInfo(ctypes.Structure):
         ("t", c_u64), ("psi_t", c_u64),
         ("q", c_u64 * MAX_PRIMES), ("psi", c_u64 * MAX_PRIMES), ("delta", c_u64 * MAX_PRIMES),
         ("fused_split", c_u32), ("fused_chunks", c_u32), ("device", c_int),
+        ("arith", c_u32), ("f64_red_every", c_u32),
     ]
 
 

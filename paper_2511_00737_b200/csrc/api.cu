@@ -142,6 +142,7 @@ void ephdc_ctx_free(ephdc_ctx *c) {
     if (c->device >= 0) {
         cudaSetDevice(c->device);
         cudaFree(c->dev.tw_q);
+        cudaFree(c->dev.tw_f64);
         cudaFree(c->dev.itw_t);
         cudaFree(c->dev.cdt);
     }
@@ -208,6 +209,11 @@ ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out
         c->fused_G = (uint32_t)((p->D_live + chunks - 1) / chunks);
         c->fused_chunks = (p->D_live + c->fused_G - 1) / c->fused_G;
     }
+    if (p->arith > EPHDC_ARITH_F64) return EPHDC_EPARAM;
+    if (p->arith != EPHDC_ARITH_INT) {
+        const bool ok = plan_f64(c->q, p->t, p->log2N, &c->f64);
+        if (!ok && p->arith == EPHDC_ARITH_F64) return EPHDC_EPARAM;
+    }
     c->device = device;
     if (device >= 0) {
         int ndev = 0;
@@ -217,6 +223,27 @@ ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out
         for (uint32_t j = 0; j < c->L; ++j) {
             auto tj = make_tw64(c->psi[j], c->q[j], p->log2N);
             std::copy(tj.begin(), tj.end(), twq.begin() + (size_t)j * N);
+        }
+        if (c->f64.enabled) {
+            // (psi_rev[i], fl(psi_rev[i] / q_j)): exact integers < 2^50 and correctly rounded quotients
+            std::vector<double> twd((size_t)c->L * N * 2);
+            for (size_t i = 0; i < (size_t)c->L * N; ++i) {
+                const double qd = (double)c->q[i / N];
+                twd[2 * i] = (double)twq[i].w;
+                twd[2 * i + 1] = (double)twq[i].w / qd;
+                if (i % N == 0) {  // index 0 is never a twiddle: it carries (q_j, fl(1/q_j))
+                    twd[2 * i] = qd;
+                    twd[2 * i + 1] = 1.0 / qd;
+                }
+            }
+            if (cudaMalloc(&c->dev.tw_f64, sizeof(double) * twd.size()) != cudaSuccess) {
+                ephdc_ctx_free(c.release());
+                return EPHDC_ERESOURCE;
+            }
+            if (cudaMemcpy(c->dev.tw_f64, twd.data(), sizeof(double) * twd.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+                ephdc_ctx_free(c.release());
+                return EPHDC_ECUDA;
+            }
         }
         std::vector<uint64_t> ipw(N);
         pow_brev(invmod(c->psi_t, p->t), p->t, p->log2N, ipw.data());
@@ -255,6 +282,8 @@ ephdc_status ephdc_ctx_query(const ephdc_ctx *c, ephdc_ctx_info *info) {
     info->fused_split = c->fused_S;
     info->fused_chunks = c->fused_chunks;
     info->device = c->device;
+    info->arith = c->f64.enabled ? EPHDC_ARITH_F64 : EPHDC_ARITH_INT;
+    info->f64_red_every = c->f64.enabled ? c->f64.red_every : 0u;
     return EPHDC_OK;
 }
 
@@ -371,7 +400,15 @@ ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_w
     ws->max_nq = max_nq;
     ws->nb_max = (max_nq + c->B - 1) / c->B;
     const size_t D = c->p.D_live;
-    if (dev_alloc(&ws->d_M, D * c->N) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
+    // FP64 path: the encoded plaintexts of all batches are kept (one fused launch over
+    // every batch), up to a 32 GB cap; the integer path keeps one batch.
+    ws->m_batches = 1;
+    if (c->f64.enabled) {
+        const size_t per = D * c->N * sizeof(uint32_t);
+        const size_t cap = std::max<size_t>(1, (32ull << 30) / per);
+        ws->m_batches = (uint32_t)std::min<size_t>(std::min<size_t>(ws->nb_max, cap), 65535);
+    }
+    if (dev_alloc(&ws->d_M, D * c->N * ws->m_batches) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
         dev_alloc(&ws->d_H, D * max_nq) != cudaSuccess ||
         dev_alloc(&ws->d_out, (size_t)ws->nb_max * 2 * c->L * c->N) != cudaSuccess) {
         ephdc_workspace_free(ws.release());
@@ -448,10 +485,31 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
     const size_t per = (size_t)2 * c->L * c->N;
     if (nb == 0) return EPHDC_OK;
     EPHDC_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(uint64_t) * per * nb, st));
+    if (c->f64.enabled) {
+        // FP64 path: pack + INTT_t of a group of batches, then ONE fused launch over the group
+        for (uint32_t b0 = 0; b0 < nb; b0 += ws->m_batches) {
+            const uint32_t g = std::min(ws->m_batches, nb - b0);
+            {
+                Timer tm(ws, st, kClsPack);
+                EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b0, g, 0, c->p.D_live, ws->d_M, st));
+                tm.done();
+            }
+            {
+                Timer tm(ws, st, kClsMac);
+                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->d_M, g, m->d_ct, d_out + per * b0, st));
+                tm.done();
+            }
+        }
+        Timer tm(ws, st, kClsFinal);
+        EPHDC_CUDA_TRY(launch_reduce_out(c, d_out, nb, st));
+        tm.done();
+        ws->last_stream = st;
+        return EPHDC_OK;
+    }
     for (uint32_t b = 0; b < nb; ++b) {
         {
             Timer tm(ws, st, kClsPack);
-            EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, 0, c->p.D_live, ws->d_M, st));
+            EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, 1, 0, c->p.D_live, ws->d_M, st));
             tm.done();
         }
         {
@@ -486,8 +544,10 @@ ephdc_status ephdc_encode_plaintexts(const ephdc_ctx *c, ephdc_workspace *ws, co
     if ((uint64_t)b * c->B >= nq || (uint64_t)d0 + nd > c->p.D_live) return EPHDC_EPARAM;
     EPHDC_CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
-    EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, d0, nd, ws->d_M, st));
-    EPHDC_CUDA_TRY(launch_plaintext_ntt(c, ws->d_M, nd, d_pt, st));
+    if (nd > c->p.D_live * ws->m_batches) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, 1, d0, nd, ws->d_M, st));
+    if (c->f64.enabled) EPHDC_CUDA_TRY(launch_plaintext_ntt_f64(c, ws->d_M, nd, d_pt, st));
+    else EPHDC_CUDA_TRY(launch_plaintext_ntt(c, ws->d_M, nd, d_pt, st));
     return EPHDC_OK;
 }
 

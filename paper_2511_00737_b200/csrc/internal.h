@@ -25,7 +25,26 @@ struct PrimeSet {
     u64 mask[kMaxL];   // 2^ceil(log2 q) - 1 (rejection sampling, reading #8)
 };
 
+// Arguments of the FP64-pipe fused kernel (kernels_f64.cu).
+struct F64MacArgs {
+    double two52_plus_t;     // 2^52 + t (centered lift, modf64.cuh)
+    const double2 *tw;       // [L][N] (psi_rev[i], fl(psi_rev[i]/q_j)); entry 0 = (q_j, fl(1/q_j))
+    u32 half_t;              // (t-1)/2
+    u32 L, D;                // primes, live dims
+    u32 nb, bg;              // batches in the launch, batches per group (grid order)
+    u32 chunks, G;           // dim chunks per batch, dims per chunk
+    u32 red_every;           // accumulator reduction interval (dims)
+};
+
+// FP64 path plan: chosen at context creation when every q_j < 2^50 and the value
+// bounds of DESIGN.md "FP64 modular arithmetic" hold.
+struct F64Plan {
+    bool enabled = false;
+    u32 red_every = 1;       // accumulator reduction interval
+};
+
 struct ctxDev {
+    double2 *tw_f64 = nullptr;     // [L][N] (w, w/q) for the FP64 path
     TwPair<u64> *tw_q = nullptr;   // [L][N] forward twiddles mod q_j
     TwPair<u32> *itw_t = nullptr;  // [N] inverse twiddles mod t
     u64 *cdt = nullptr;            // [20]
@@ -50,6 +69,7 @@ struct ephdc_ctx {
     int device = -1;
     ephdc::ctxDev dev;
     uint32_t fused_S = 1, fused_chunks = 1, fused_G = 1;
+    ephdc::F64Plan f64;
 };
 
 struct ephdc_sk {
@@ -67,7 +87,8 @@ struct ephdc_model {
 struct ephdc_workspace {
     const ephdc_ctx *ctx = nullptr;
     uint32_t max_nq = 0;
-    uint32_t *d_M = nullptr;      // [D_live][N] encoded plaintexts (mod t) of one batch
+    uint32_t *d_M = nullptr;      // [m_batches][D_live][N] encoded plaintexts (mod t)
+    uint32_t m_batches = 1;       // batches d_M holds (FP64 path: all of max_nq, capped)
     void *d_X = nullptr;          // [max_nq][F]
     int8_t *d_H = nullptr;        // [D_live][max_nq]
     uint64_t *d_out = nullptr;    // [nb_max][2][L][N]
@@ -98,8 +119,9 @@ extern std::atomic<uint64_t> g_launches;
 // ---- launchers (kernels.cu); all return cudaGetLastError() after the launch ----
 cudaError_t launch_encode(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, void *d_H, bool raw,
                           cudaStream_t st);
-cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t d0,
-                                     uint32_t nd, uint32_t *d_M, cudaStream_t st);
+// slot pack + INTT_t of batches [b, b+nbat) x dims [d0, d0+nd) -> d_M [nbat][nd][N]
+cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t nbat,
+                                     uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st);
 cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
                                    cudaStream_t st);
 cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64_t *d_model, uint64_t *d_out,
@@ -114,6 +136,15 @@ cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_
 cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
                        uint64_t *d_out, cudaStream_t st);
 size_t ntt_mac_smem_bytes(uint32_t log2Nc);
+// FP64-pipe path (kernels_f64.cu)
+cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const uint64_t *d_model,
+                               uint64_t *d_out, cudaStream_t st);
+cudaError_t launch_plaintext_ntt_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
+                                     cudaStream_t st);
+cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, cudaStream_t st);
+int ntt_mac_f64_occupancy(uint32_t log2N);
+bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan);
+void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G);
 int ntt_mac_occupancy(uint32_t log2N, uint32_t S);
 
 }  // namespace ephdc

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__((1 << LG) / kE)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u32 *buf = reinterpret_cast<u32 *>(smem_raw);
     const u32 d = d0 + blockIdx.x;
+    b += blockIdx.y;  // grid.y = consecutive batches, written to M[blockIdx.y][blockIdx.x]
     u32 lim;
     const int8_t *row;
     if constexpr (MODEL) {
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__((1 << LG) / kE)
         return v < 0 ? (u32)((int)t + v) : (u32)v;
     };
     inv_ntt<u32, LG, kE>(buf, load, a.itw, t);
-    u32 *out = M + (size_t)blockIdx.x * N;
+    u32 *out = M + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * N;
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
         const int pos = threadIdx.x + e * NT;
@@ -396,38 +397,39 @@ static PackArgs pack_args(const ephdc_ctx *c) {
 }
 
 template <int LG, bool MODEL>
-static cudaError_t pack_launch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 d0, u32 nd, u32 *M,
+static cudaError_t pack_launch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 nbat, u32 d0, u32 nd, u32 *M,
                                cudaStream_t st) {
     const size_t smem = sizeof(u32) * padded_len(1 << LG);
     auto kern = k_pack_intt<LG, MODEL>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    kern<<<nd, (1 << LG) / kE, smem, st>>>(src, nq, b, d0, pack_args(c), M);
+    kern<<<dim3(nd, nbat), (1 << LG) / kE, smem, st>>>(src, nq, b, d0, pack_args(c), M);
     return counted(cudaGetLastError());
 }
 
 template <bool MODEL>
-static cudaError_t pack_dispatch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 d0, u32 nd, u32 *M,
-                                 cudaStream_t st) {
-    if (nd == 0) return cudaSuccess;
+static cudaError_t pack_dispatch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 nbat, u32 d0, u32 nd,
+                                 u32 *M, cudaStream_t st) {
+    if (nd == 0 || nbat == 0) return cudaSuccess;
+    if (nbat > 65535) return cudaErrorInvalidConfiguration;
     switch (c->p.log2N) {
-        case 10: return pack_launch<10, MODEL>(c, src, nq, b, d0, nd, M, st);
-        case 11: return pack_launch<11, MODEL>(c, src, nq, b, d0, nd, M, st);
-        case 12: return pack_launch<12, MODEL>(c, src, nq, b, d0, nd, M, st);
-        case 13: return pack_launch<13, MODEL>(c, src, nq, b, d0, nd, M, st);
-        case 14: return pack_launch<14, MODEL>(c, src, nq, b, d0, nd, M, st);
+        case 10: return pack_launch<10, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 11: return pack_launch<11, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 12: return pack_launch<12, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 13: return pack_launch<13, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 14: return pack_launch<14, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
     }
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t d0,
-                                     uint32_t nd, uint32_t *d_M, cudaStream_t st) {
-    return pack_dispatch<false>(c, d_H, nq, b, d0, nd, d_M, st);
+cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t nbat,
+                                     uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st) {
+    return pack_dispatch<false>(c, d_H, nq, b, nbat, d0, nd, d_M, st);
 }
 
 cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
                                    cudaStream_t st) {
-    return pack_dispatch<true>(c, d_C, 0, 0, d0, nd, d_M, st);
+    return pack_dispatch<true>(c, d_C, 0, 0, 1, d0, nd, d_M, st);
 }
 
 static MacArgs mac_args(const ephdc_ctx *c) {

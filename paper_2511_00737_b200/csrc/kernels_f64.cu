@@ -1,0 +1,342 @@
+// kernels_f64.cu -- the FP64-pipe variant of the dominant fused kernel (primes q < 2^50).
+//
+//  k_ntt_mac_f64   centered lift (#3) + forward NTT mod q_j + ct x pt MAC
+//                  for ALL batches of a call in one launch; accumulators in registers
+//  k_pt_ntt_f64    the same NTT, canonical outputs stored (parity export of p_hat)
+//  k_reduce_out    out mod q_j (the atomically folded partial sums)
+//
+// Work item (one CTA) = (batch b, prime j, slice s of S, chunk of G dims).  Items are
+// ordered [batch group][chunk][batch in group][prime][slice] so the ~148 CTAs resident
+// at a time share their chunk's model tiles (read by every batch of the group) and
+// encoded plaintexts (read by every prime and slice) through L2: the 23.6 GB model of
+// c4 crosses HBM once per batch group instead of once per batch.  DESIGN.md "Kernels".
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "internal.h"
+#include "ntt_f64.cuh"
+
+namespace ephdc {
+
+using namespace ephdc_f64;
+
+namespace {
+
+EPHDC_D void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+EPHDC_D ulonglong2 ld_pair(const u64 *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
+
+inline cudaError_t counted(cudaError_t e) {
+    if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+    return e;
+}
+
+}  // namespace
+
+// 512 threads x 128 registers per SM: one CTA at NC = 8192, two at 4096, ...
+#define EPHDC_F64_BOUNDS(LGC) __launch_bounds__((1 << (LGC)) / kE, (8192 >> (LGC)) > 1 ? (8192 >> (LGC)) : 1)
+
+template <int LGC, int S>
+__global__ void EPHDC_F64_BOUNDS(LGC)
+    k_ntt_mac_f64(const u32 *__restrict__ M, const u64 *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
+    constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *tw = reinterpret_cast<double2 *>(smem_raw);              // [NC]
+    double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * NC);
+    const int tid = threadIdx.x;
+    u32 x = blockIdx.x;
+    const u32 s = x % S;
+    x /= S;
+    const u32 j = x % a.L;
+    x /= a.L;
+    const u32 bl = x % a.bg;
+    x /= a.bg;
+    const u32 chunk = x % a.chunks, grp = x / a.chunks;
+    const u32 b = grp * a.bg + bl;
+    if (b >= a.nb) return;
+    const u32 d0 = chunk * a.G, d1 = min(a.D, d0 + a.G);
+    if (d0 >= d1) return;
+
+    const double2 *twg = a.tw + (size_t)j * N;
+    const double2 qq = twg[0];  // slot 0 of the table holds (q_j, fl(1/q_j))
+    const double q = qq.x, nq = -q, qinv = qq.y;
+    for (int i = tid; i < NC; i += NT) {
+        if (i == 0) {
+            tw[0] = make_double2(0.0, 0.0);
+            continue;
+        }
+        const int m = 1 << (31 - __clz(i));
+        tw[i] = twg[S * m + (int)s * m + (i - m)];
+    }
+    double2 w1 = make_double2(0.0, 0.0);
+    if constexpr (S > 1) w1 = twg[1];
+    __syncthreads();
+
+    double acc0[kE], acc1[kE];
+#pragma unroll
+    for (int e = 0; e < kE; ++e) acc0[e] = acc1[e] = 0.0;
+    const u32 half_t = a.half_t;
+    const double two52t = a.two52_plus_t;
+    u32 since_red = 0;
+    for (u32 d = d0; d < d1; ++d) {
+        const u32 *m = M + ((size_t)b * a.D + d) * N;
+        const u64 *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
+        const u64 *c1 = c0 + N;
+        // L2 prefetch: this dim's model slice (read by the final pass) and the next
+        // dim's plaintext row (read by the first pass of the next iteration)
+        prefetch_l2(c0 + 16 * tid);
+        prefetch_l2(c1 + 16 * tid);
+        if (d + 1 < d1 && tid * 32 < N) prefetch_l2(m + N + 32 * tid);
+        auto load = [&](int pos) -> double {
+            const double U = lift_centered(__ldg(m + pos), half_t, two52t);
+            if constexpr (S == 1) {
+                return U;
+            } else {
+                // first global stage (half-size N/2) fused into the load: slice s keeps U +- w V
+                const double V = lift_centered(__ldg(m + pos + NC), half_t, two52t);
+                const double T = mul_tw(V, w1.x, w1.y, nq);
+                return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
+            }
+        };
+        auto mac = [&](int u, int g, double x0, double x1) {
+            const ulonglong2 a0 = ld_pair(c0 + 2 * g), a1 = ld_pair(c1 + 2 * g);
+            acc0[2 * u] = __dadd_rn(acc0[2 * u], mul_rt(from_u64(a0.x), x0, qinv, nq));
+            acc0[2 * u + 1] = __dadd_rn(acc0[2 * u + 1], mul_rt(from_u64(a0.y), x1, qinv, nq));
+            acc1[2 * u] = __dadd_rn(acc1[2 * u], mul_rt(from_u64(a1.x), x0, qinv, nq));
+            acc1[2 * u + 1] = __dadd_rn(acc1[2 * u + 1], mul_rt(from_u64(a1.y), x1, qinv, nq));
+        };
+        fwd_ntt<LGC>(buf, load, tw, nq, mac);
+        if (++since_red >= a.red_every) {
+            since_red = 0;
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                acc0[e] = reduce(acc0[e], qinv, nq);
+                acc1[e] = reduce(acc1[e], qinv, nq);
+            }
+        }
+        __syncthreads();  // the next first pass overwrites buf
+    }
+    // fold this chunk's sum (canonical, < q) into the batch's scores ciphertext; the
+    // sums of <= chunks values < q fit 64 bits (checked on the host) and integer
+    // addition is order-independent, so the result is deterministic
+    u64 *o0 = out + (((size_t)b * 2 + 0) * a.L + j) * N + (size_t)s * NC;
+    u64 *o1 = out + (((size_t)b * 2 + 1) * a.L + j) * N + (size_t)s * NC;
+#pragma unroll
+    for (int u = 0; u < kE / 2; ++u) {
+        const int g = tid + u * NT;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const u64 v0 = to_canonical_u64(reduce(acc0[2 * u + e], qinv, nq), q);
+            const u64 v1 = to_canonical_u64(reduce(acc1[2 * u + e], qinv, nq), q);
+            atomicAdd(reinterpret_cast<unsigned long long *>(o0 + 2 * g + e), (unsigned long long)v0);
+            atomicAdd(reinterpret_cast<unsigned long long *>(o1 + 2 * g + e), (unsigned long long)v1);
+        }
+    }
+}
+
+// Plaintext NTTs for the parity export: p_hat[dd][j] = NTT_j(lift(M[dd])), canonical.
+// CTA = (dim dd, prime j, slice s); same passes as the fused kernel.
+template <int LGC, int S>
+__global__ void EPHDC_F64_BOUNDS(LGC)
+    k_pt_ntt_f64(const u32 *__restrict__ M, u64 *__restrict__ pt, F64MacArgs a) {
+    constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *tw = reinterpret_cast<double2 *>(smem_raw);
+    double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * NC);
+    const int tid = threadIdx.x;
+    u32 x = blockIdx.x;
+    const u32 s = x % S;
+    x /= S;
+    const u32 j = x % a.L, dd = x / a.L;
+    const double2 *twg = a.tw + (size_t)j * N;
+    const double2 qq = twg[0];  // slot 0 of the table holds (q_j, fl(1/q_j))
+    const double q = qq.x, nq = -q, qinv = qq.y;
+    for (int i = tid; i < NC; i += NT) {
+        if (i == 0) {
+            tw[0] = make_double2(0.0, 0.0);
+            continue;
+        }
+        const int m = 1 << (31 - __clz(i));
+        tw[i] = twg[S * m + (int)s * m + (i - m)];
+    }
+    double2 w1 = make_double2(0.0, 0.0);
+    if constexpr (S > 1) w1 = twg[1];
+    __syncthreads();
+    const u32 *m = M + (size_t)dd * N;
+    const u32 half_t = a.half_t;
+    const double two52t = a.two52_plus_t;
+    auto load = [&](int pos) -> double {
+        const double U = lift_centered(m[pos], half_t, two52t);
+        if constexpr (S == 1) {
+            return U;
+        } else {
+            const double V = lift_centered(m[pos + NC], half_t, two52t);
+            const double T = mul_tw(V, w1.x, w1.y, nq);
+            return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
+        }
+    };
+    u64 *o = pt + ((size_t)dd * a.L + j) * N + (size_t)s * NC;
+    auto store = [&](int, int g, double x0, double x1) {
+        ulonglong2 v;
+        v.x = to_canonical_u64(reduce(x0, qinv, nq), q);
+        v.y = to_canonical_u64(reduce(x1, qinv, nq), q);
+        *reinterpret_cast<ulonglong2 *>(o + 2 * g) = v;
+    };
+    fwd_ntt<LGC>(buf, load, tw, nq, store);
+}
+
+// out[b][c][j][i] <- out mod q_j
+__global__ void k_reduce_out(u64 *__restrict__ out, u32 L, u32 N, PrimeSet ps, size_t n_total) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_total) return;
+    const u32 j = (u32)((i / N) % L);
+    out[i] %= ps.q[j];
+}
+
+// ------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------
+size_t ntt_f64_smem_bytes(uint32_t lgc) {
+    const size_t nc = (size_t)1 << lgc;
+    return sizeof(double2) * nc + sizeof(double) * (size_t)ephdc_f64::padded_len((int)nc);
+}
+
+static F64MacArgs f64_args(const ephdc_ctx *c) {
+    F64MacArgs a{};
+    a.half_t = (u32)((c->t - 1) / 2);
+    a.two52_plus_t = 4503599627370496.0 + (double)c->t;
+    a.L = c->L;
+    a.D = c->p.D_live;
+    a.red_every = c->f64.red_every;
+    a.tw = c->dev.tw_f64;
+    return a;
+}
+
+template <class K> static cudaError_t smem_attr(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int LGC, int S>
+static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb, const u64 *model, u64 *out,
+                                  cudaStream_t st) {
+    const size_t smem = ntt_f64_smem_bytes(LGC);
+    auto kern = k_ntt_mac_f64<LGC, S>;
+    cudaError_t e = smem_attr(kern, smem);
+    if (e != cudaSuccess) return e;
+    F64MacArgs a = f64_args(c);
+    a.nb = nb;
+    f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
+    const uint64_t groups = (nb + a.bg - 1) / a.bg;
+    const uint64_t grid = groups * a.chunks * a.bg * c->L * S;
+    if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+    kern<<<(unsigned)grid, (1 << LGC) / kE, smem, st>>>(M, model, out, a);
+    return counted(cudaGetLastError());
+}
+
+
+cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const uint64_t *d_model,
+                               uint64_t *d_out, cudaStream_t st) {
+    if (nb == 0) return cudaSuccess;
+    switch (c->p.log2N) {
+        case 10: return mac_f64_launch<10, 1>(c, d_M, nb, d_model, d_out, st);
+        case 11: return mac_f64_launch<11, 1>(c, d_M, nb, d_model, d_out, st);
+        case 12: return mac_f64_launch<12, 1>(c, d_M, nb, d_model, d_out, st);
+        case 13: return mac_f64_launch<13, 1>(c, d_M, nb, d_model, d_out, st);
+        case 14: return mac_f64_launch<13, 2>(c, d_M, nb, d_model, d_out, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int LGC, int S>
+static cudaError_t pt_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nd, u64 *pt, cudaStream_t st) {
+    const size_t smem = ntt_f64_smem_bytes(LGC);
+    auto kern = k_pt_ntt_f64<LGC, S>;
+    cudaError_t e = smem_attr(kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<nd * c->L * S, (1 << LGC) / kE, smem, st>>>(M, pt, f64_args(c));
+    return counted(cudaGetLastError());
+}
+
+
+cudaError_t launch_plaintext_ntt_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
+                                     cudaStream_t st) {
+    if (nd == 0) return cudaSuccess;
+    switch (c->p.log2N) {
+        case 10: return pt_f64_launch<10, 1>(c, d_M, nd, d_pt, st);
+        case 11: return pt_f64_launch<11, 1>(c, d_M, nd, d_pt, st);
+        case 12: return pt_f64_launch<12, 1>(c, d_M, nd, d_pt, st);
+        case 13: return pt_f64_launch<13, 1>(c, d_M, nd, d_pt, st);
+        case 14: return pt_f64_launch<13, 2>(c, d_M, nd, d_pt, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, cudaStream_t st) {
+    const size_t n = (size_t)nb * 2 * c->L * c->N;
+    if (n == 0) return cudaSuccess;
+    k_reduce_out<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_out, c->L, c->N, c->ps, n);
+    return counted(cudaGetLastError());
+}
+
+int ntt_mac_f64_occupancy(uint32_t log2N) {
+    const uint32_t lgc = log2N > 13 ? 13 : log2N;
+    const int occ = 8192 >> lgc;  // EPHDC_F64_BOUNDS; shared memory allows the same
+    return occ < 1 ? 1 : occ;
+}
+
+// Value bounds of the FP64 path: every input of
+// mul_tw below 2^51, every MAC operand |a b / q| below 2^51, accumulators below 2^53.
+bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan) {
+    *plan = F64Plan{};
+    const double L51 = 0.98 * 2251799813685248.0, L53 = 0.98 * 9007199254740992.0, e54 = 1.0 / 18014398509481984.0;
+    const uint32_t S = log2N >= 14 ? 2 : 1, lgc = log2N - (S - 1);
+    u32 red_every = 1u << 20;
+    for (uint64_t qj : q) {
+        if (qj >= (1ull << 50)) return false;
+        const double Q = (double)qj;
+        auto rtw = [&](double X) { return (0.5 + X * e54) * Q + 2.0; };  // |mul_tw| bound
+        double B = (double)((t - 1) / 2);                                // centered lift
+        for (uint32_t st = 0; st < lgc + (S - 1); ++st) {                // every CT stage
+            if (B >= L51) return false;
+            B += rtw(B);
+        }
+        if (B >= L51) return false;                                      // MAC operand
+        const double rmac = (0.5 + 2.0 * B * e54 * 2.0) * Q + 2.0;       // |mul_rt| bound
+        const double n = std::floor((L53 - (Q / 2 + 2.0)) / rmac);
+        if (n < 1) return false;
+        red_every = std::min<u32>(red_every, (u32)std::min(n, 1048576.0));
+    }
+    plan->enabled = true;
+    plan->red_every = red_every;
+    return true;
+}
+
+// Grid of one fused launch over nb batches: batches per group so a group's items of
+// one chunk fill the GPU once (model tiles shared through L2), and the chunk count
+// that minimises waves x dims-per-item.
+void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G) {
+    const uint32_t S = c->p.log2N >= 14 ? 2 : 1;
+    const uint64_t W = 148ull * ntt_mac_f64_occupancy(c->p.log2N);
+    const uint64_t LS = (uint64_t)c->L * S;
+    const uint32_t D = c->p.D_live;
+    *bg = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nb, W / LS));
+    const uint64_t real = (uint64_t)nb * LS;
+    uint64_t best = ~0ull;
+    uint32_t best_c = 1;
+    const uint32_t cmax = std::min<uint32_t>(D, 1024);
+    for (uint32_t ch = 1; ch <= cmax; ++ch) {
+        const uint64_t g = (D + ch - 1) / ch;
+        const uint64_t waves = (real * ch + W - 1) / W;
+        const uint64_t cost = waves * (g + 1);
+        if (cost < best) {
+            best = cost;
+            best_c = ch;
+        }
+    }
+    *G = (D + best_c - 1) / best_c;
+    *chunks = (D + *G - 1) / *G;
+}
+
+}  // namespace ephdc

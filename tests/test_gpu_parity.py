@@ -26,15 +26,18 @@ from paper_2511_00737_b200 import pipeline as ppipe  # noqa: E402
 _CACHE = {}
 
 
-def setup(name, nq):
-    key = (name, nq)
+ARITH = {"auto": 0, "int": 1, "f64": 2}
+
+
+def setup(name, nq, arith="auto"):
+    key = (name, nq, arith)
     if key in _CACHE:
         return _CACHE[key]
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, yq = inp.gen_features(cfg, nq)
     P = inp.gen_projection(cfg)
     om = opipe.build_model(cfg, P, Xtr, ytr)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, arith=ARITH[arith])
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H_dev = eph.encode_queries(ps.ctx, X, ps.P_dev)
     torch.cuda.synchronize()
@@ -48,12 +51,25 @@ def _u64(t):
     return t.cpu().numpy().view(np.uint64)
 
 
-CASES = [("c1", 16), ("c1q3", 16), ("c1q3", 700), ("c2", 1024), ("c2", 2100), ("c3", 900)]
+CASES = [("c1", 16, "auto"), ("c1q3", 16, "auto"), ("c1q3", 700, "auto"), ("c2", 1024, "auto"), ("c2", 2100, "auto"),
+         ("c3", 900, "auto"),
+         # the integer-pipe kernel (used when a prime is >= 2^50) on the same workloads
+         ("c1q3", 700, "int"), ("c2", 2100, "int"), ("c3", 900, "int")]
 
 
-@pytest.mark.parametrize("name,nq", CASES)
-def test_model_build_and_encoding_bitexact(name, nq):
-    r = setup(name, nq)
+def test_arith_selection():
+    # every BASELINE.json config has primes < 2^50: AUTO selects the FP64 pipe;
+    # c4 (48-bit primes, N = 16384) needs the mid-NTT reduction
+    for name in ("c1", "c1q3", "c2", "c3"):
+        r = setup(name, 16)
+        assert r["ps"].ctx.arith == "f64", name
+        assert r["ps"].ctx.info.f64_red_every >= 1
+    assert setup("c2", 2100, "int")["ps"].ctx.arith == "int"
+
+
+@pytest.mark.parametrize("name,nq,arith", CASES)
+def test_model_build_and_encoding_bitexact(name, nq, arith):
+    r = setup(name, nq, arith)
     assert r["ps"].Qbits == r["om"].Qbits and r["ps"].qshift == r["om"].qshift
     assert np.array_equal(r["ps"].class_hv, r["om"].class_hv)
     assert np.array_equal(r["H_dev"].cpu().numpy(), r["H_or"])
@@ -69,9 +85,10 @@ def test_model_ciphertexts_bitexact(name, nq):
         assert np.array_equal(got, want), (d0, nd)
 
 
-@pytest.mark.parametrize("name,nq", [("c1q3", 700), ("c2", 2100), ("c3", 900)])
-def test_plaintext_ntts_bitexact(name, nq):
-    r = setup(name, nq)
+@pytest.mark.parametrize("name,nq,arith", [("c1q3", 700, "auto"), ("c2", 2100, "auto"), ("c3", 900, "auto"),
+                                          ("c2", 2100, "int"), ("c3", 900, "int")])
+def test_plaintext_ntts_bitexact(name, nq, arith):
+    r = setup(name, nq, arith)
     ps, om = r["ps"], r["om"]
     ws = eph.Workspace(ps.ctx, nq)
     nb = ps.ctx.n_batches(nq)
@@ -82,9 +99,9 @@ def test_plaintext_ntts_bitexact(name, nq):
             assert np.array_equal(got, want), (b, d0)
 
 
-@pytest.mark.parametrize("name,nq", CASES)
-def test_infer_bitexact_and_decrypts_to_dot_products(name, nq):
-    r = setup(name, nq)
+@pytest.mark.parametrize("name,nq,arith", CASES)
+def test_infer_bitexact_and_decrypts_to_dot_products(name, nq, arith):
+    r = setup(name, nq, arith)
     ps, om = r["ps"], r["om"]
     ws = eph.Workspace(ps.ctx, nq)
     cts = eph.infer_batch(ps.ctx, ps.model, ws, r["H_dev"], nq)
