@@ -31,9 +31,16 @@ sys.path.insert(0, ROOT)
 import ephdc_inputs as inp  # noqa: E402
 
 METRIC = "encrypted-HDC queries/sec on 1 B200; NTT+MAC fraction of HBM/int roofline"
-# Integer-pipe peak: 148 SMs x 64 IMAD lanes/clk (fma pipe,
-# rt_SMSP = 2, B300_MICROARCH.md) x max SM clock, / 10 multiply instructions per u64
-# Shoup/Montgomery modular multiply on the 32-bit multiplier.
+# Roofline of the dominant kernel.  FP64 path: the pipe is the
+# FP64 unit, 64 DFMA-class lanes/clk/SM (profiles/r01/int_peak.jsonl measures 63.1);
+# the algorithmic work of a launch is its butterflies and MAC products at the minimum
+# instruction count of the exact double arithmetic (modf64.cuh): 8 per butterfly
+# (one exact product = 6, plus the add and the subtract), 7 per MAC term (product +
+# accumulate).  Integer path: 64 IMAD lanes/clk/SM, 10 multiply instructions per u64
+# Shoup/Montgomery product.
+FP64_PER_SM_CLK = 64
+F64_OPS_PER_BFLY = 8
+F64_OPS_PER_MAC = 7
 IMAD_PER_SM_CLK = 64
 IMAD_PER_MULMOD = 10
 
@@ -212,12 +219,17 @@ def main():
     n0 = eph.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    enc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     e0.record(stream)
-    for _ in range(a.steps):
-        step()
+    for i in range(a.steps):
+        enc_ev[i][0].record(stream)
+        eph.encode_queries(ctx, X_dev, ps.P_dev, H)
+        enc_ev[i][1].record(stream)
+        eph.infer_batch(ctx, model, ws, H, nq, out)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     launches = eph.launch_count() - n0
+    enc_ms = sum(x.elapsed_time(y) for x, y in enc_ev)
     kt = ws.timing()
     ws.set_timing(False)
     clk = clocks.stop()
@@ -230,18 +242,39 @@ def main():
     ms_max = float(t.item())
     value = world * nq / (ms_max / 1e3)
 
-    # roofline of the dominant kernel: the fused lift + NTT_q + MAC (one launch per batch)
+    # roofline of the dominant kernel: the fused lift + NTT_q + MAC (all batches per launch)
     mac_ms, mac_n = kt["ntt_mac"]
-    per_launch_s = mac_ms / max(1, mac_n) / 1e3
+    mac_s = mac_ms / a.steps / 1e3                              # per step
     N, L, D = ctx.N, ctx.L, cfg.D_live
-    mulmods = D * L * ((N // 2) * cfg.log2N + 2 * N)      # butterflies + 2 MAC products per coefficient
-    achieved = mulmods / per_launch_s / 1e9
+    bfly = nb * D * L * (N // 2) * cfg.log2N                    # butterflies per step
+    macs = nb * D * L * 2 * N                                   # MAC products per step
     smax = measured_peaks().get("sm_max_mhz") or 1965.0
-    peak = 148 * IMAD_PER_SM_CLK * smax * 1e6 / IMAD_PER_MULMOD / 1e9
+    if ctx.arith == "f64":
+        achieved = (F64_OPS_PER_BFLY * bfly + F64_OPS_PER_MAC * macs) / mac_s / 1e9
+        peak = 148 * FP64_PER_SM_CLK * smax * 1e6 / 1e9
+        unit, kname = "GFP64op/s", "k_ntt_mac_f64"
+        src = ("derived: 148 SMs x 64 FP64 lanes/clk x sm_max_mhz; work = 8 ops/butterfly + 7 ops/MAC "
+               "term of the exact double arithmetic (DESIGN.md)")
+    else:
+        achieved = (bfly + macs) / mac_s / 1e9
+        peak = 148 * IMAD_PER_SM_CLK * smax * 1e6 / IMAD_PER_MULMOD / 1e9
+        unit, kname = "Gmulmod/s", "k_ntt_mac"
+        src = "derived: 148 SMs x 64 IMAD/clk x sm_max_mhz / 10 IMAD per u64 mulmod (DESIGN.md)"
+    kt["encode"] = (enc_ms, a.steps)
     total_ms = sum(v[0] for v in kt.values())
-    roofline = {"bound": "alu", "kernel": "k_ntt_mac", "achieved": round(achieved, 1), "peak": round(peak, 1),
-                "unit": "Gmulmod/s", "frac": round(achieved / peak, 4), "traffic": None,
-                "peak_source": "derived: 148 SMs x 64 IMAD/clk x sm_max_mhz / 10 IMAD per u64 mulmod (DESIGN.md)",
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(cfg.name)
+        if tr and tr.get("kernel") == kname:
+            traffic = tr["bytes_per_step"]
+    except Exception:
+        pass
+    roofline = {"bound": "alu", "kernel": kname, "achieved": round(achieved, 1), "peak": round(peak, 1),
+                "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic": {"butterflies_per_step": bfly, "mac_terms_per_step": macs,
+                                "model_bytes": D * L * 2 * N * 8, "launches_per_step": mac_n / a.steps},
+                "mulmod_rate_G_per_s": round((bfly + macs) / mac_s / 1e9, 1),
+                "peak_source": src,
                 "share_of_step": round(mac_ms / max(total_ms, 1e-9), 4),
                 "kernel_ms": {k: round(v[0] / a.steps, 3) for k, v in kt.items()}}
 
@@ -275,12 +308,12 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64" if ctx.arith == "f64" else "u64", "data": "synthetic",
                 "config": {"workload": cfg.name, "nq_per_gpu": nq, "batches": nb, "N": N, "L": L, "D": D,
                            "k": cfg.k, "F": cfg.F, "t": ctx.t, "log2q": sum(int(q).bit_length() for q in ctx.q),
                            "parallelism": f"replica x{world} (independent query batches)",
-                           "l2": "inputs larger than L2 (encrypted model %.1f GB streamed per batch)"
-                                 % (D * L * 2 * N * 8 / 1e9)},
+                           "arith": ctx.arith,
+                           "l2": "inputs larger than L2 (encrypted model %.1f GB in HBM)" % (D * L * 2 * N * 8 / 1e9)},
                 "gpu_launches": int(launches), "clocks": clk, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e}
         print(json.dumps(line))
     if world > 1:

@@ -14,9 +14,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ntt_f64.cuh"
+#include "tmem.cuh"
+#include "async_copy.cuh"
 
 namespace ephdc {
 
@@ -35,17 +38,43 @@ inline cudaError_t counted(cudaError_t e) {
 
 }  // namespace
 
-// 512 threads x 128 registers per SM: one CTA at NC = 8192, two at 4096, ...
-#define EPHDC_F64_BOUNDS(LGC) __launch_bounds__((1 << (LGC)) / kE, (8192 >> (LGC)) > 1 ? (8192 >> (LGC)) : 1)
+// Occupancy: 512 threads x 128 registers per SM and 128 TMEM columns per warp of a lane
+// quarter (512 per SM): one CTA at NC = 8192, two at 4096, four at <= 2048.
+template <int LGC> constexpr int f64_ctas_per_sm() {
+    constexpr int by_regs = (8192 >> LGC) > 1 ? (8192 >> LGC) : 1;
+    return by_regs < 4 ? by_regs : 4;
+}
+#define EPHDC_F64_BOUNDS(LGC) __launch_bounds__((1 << (LGC)) / kE, f64_ctas_per_sm<LGC>())
+
+// TMEM columns of one CTA: 128 per warp of a lane quarter (64 accumulator columns =
+// 2 x 16 doubles, 32 last-stage twiddle columns = 8 x (w, w/q), 32 spare).
+template <int LGC> constexpr uint32_t tmem_cols() {
+    constexpr int warps = (1 << LGC) / kE / 32;
+    return 128u * (uint32_t)((warps + 3) / 4);
+}
+
+// Dynamic shared memory of the fused kernel: head-stage twiddles [NC/2] double2, the
+// NTT buffer, the staged plaintext row [S*NC] u32.
+template <int LGC, int S> constexpr size_t mac_f64_smem() {
+    constexpr size_t nc = (size_t)1 << LGC;
+    return sizeof(double2) * (nc / 2) + sizeof(double) * (size_t)ephdc_f64::padded_len((int)nc) +
+           sizeof(uint32_t) * nc * S;
+}
 
 template <int LGC, int S>
 __global__ void EPHDC_F64_BOUNDS(LGC)
     k_ntt_mac_f64(const u32 *__restrict__ M, const u64 *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
+    using namespace ephdc_async;
     constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *tw = reinterpret_cast<double2 *>(smem_raw);              // [NC]
-    double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * NC);
-    const int tid = threadIdx.x;
+    constexpr uint32_t kCols = tmem_cols<LGC>();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t mbar;
+    double2 *tw = reinterpret_cast<double2 *>(smem_raw);                               // [NC/2]
+    double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * (NC / 2));   // padded [NC]
+    u32 *mst = reinterpret_cast<u32 *>(smem_raw + sizeof(double2) * (NC / 2) +
+                                       sizeof(double) * padded_len(NC));               // [N]
+    const int tid = threadIdx.x, warp = tid >> 5;
     u32 x = blockIdx.x;
     const u32 s = x % S;
     x /= S;
@@ -59,81 +88,166 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     const u32 d0 = chunk * a.G, d1 = min(a.D, d0 + a.G);
     if (d0 >= d1) return;
 
+    const u32 *Mb = M + (size_t)b * a.D * N;
+    if (warp == 0) ephdc_tmem::alloc(&tmem_slot, kCols);
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        // first plaintext row of the chunk -> shared memory (TMA bulk copy)
+        mbar_arrive_expect_tx(&mbar, N * 4u);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) bulk_g2s(mst + c * (N / 4), Mb + (size_t)d0 * N + c * (N / 4), N, &mbar);
+    }
     const double2 *twg = a.tw + (size_t)j * N;
     const double2 qq = twg[0];  // slot 0 of the table holds (q_j, fl(1/q_j))
     const double q = qq.x, nq = -q, qinv = qq.y;
-    for (int i = tid; i < NC; i += NT) {
-        if (i == 0) {
-            tw[0] = make_double2(0.0, 0.0);
-            continue;
-        }
-        const int m = 1 << (31 - __clz(i));
-        tw[i] = twg[S * m + (int)s * m + (i - m)];
-    }
+    load_twiddles<LGC, S>(tw, twg, (int)s, NC / 2);
     double2 w1 = make_double2(0.0, 0.0);
     if constexpr (S > 1) w1 = twg[1];
+    ephdc_tmem::fence_before_sync();
     __syncthreads();
-
-    double acc0[kE], acc1[kE];
+    ephdc_tmem::fence_after_sync();
+    // this thread's TMEM columns: block c (pairs g = tid + u*NT, u = 2c, 2c+1) keeps its
+    // accumulators at 16c .. 16c+15 = (acc0[2u], acc0[2u+1], acc1[2u], acc1[2u+1]) x 2 words
+    // and its last-stage twiddles at 64 + 8c .. 64 + 8c + 7 = (w, w/q) x 2 words x 2 pairs
+    const uint32_t tacc = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u;
+    const uint32_t ttw = tacc + 64u;
+    {
+        uint32_t z[16];
 #pragma unroll
-    for (int e = 0; e < kE; ++e) acc0[e] = acc1[e] = 0.0;
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ephdc_tmem::st16(tacc + 16 * c, z);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t t[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double2 w = twg[tail_twiddle_index<LGC, S>((int)s, tid + (4 * h + k) * NT)];
+                t[4 * k] = (uint32_t)__double2loint(w.x);
+                t[4 * k + 1] = (uint32_t)__double2hiint(w.x);
+                t[4 * k + 2] = (uint32_t)__double2loint(w.y);
+                t[4 * k + 3] = (uint32_t)__double2hiint(w.y);
+            }
+            ephdc_tmem::st16(ttw + 16 * h, t);
+        }
+    }
+
     const u32 half_t = a.half_t;
     const double two52t = a.two52_plus_t;
-    u32 since_red = 0;
+    u32 since_red = 0, phase = 0;
     for (u32 d = d0; d < d1; ++d) {
-        const u32 *m = M + ((size_t)b * a.D + d) * N;
         const u64 *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
         const u64 *c1 = c0 + N;
-        // L2 prefetch: this dim's model slice (read by the final pass) and the next
-        // dim's plaintext row (read by the first pass of the next iteration)
-        prefetch_l2(c0 + 16 * tid);
-        prefetch_l2(c1 + 16 * tid);
-        if (d + 1 < d1 && tid * 32 < N) prefetch_l2(m + N + 32 * tid);
+        if (!(a.flags & 1u)) {
+            prefetch_l2(c0 + 16 * tid);  // this dim's model slice, read by the last stage
+            prefetch_l2(c1 + 16 * tid);
+        }
+        mbar_wait(&mbar, phase);     // plaintext row d is in mst
+        phase ^= 1u;
         auto load = [&](int pos) -> double {
-            const double U = lift_centered(__ldg(m + pos), half_t, two52t);
+            const double U = lift_centered(mst[pos], half_t, two52t);
             if constexpr (S == 1) {
                 return U;
             } else {
                 // first global stage (half-size N/2) fused into the load: slice s keeps U +- w V
-                const double V = lift_centered(__ldg(m + pos + NC), half_t, two52t);
+                const double V = lift_centered(mst[pos + NC], half_t, two52t);
                 const double T = mul_tw(V, w1.x, w1.y, nq);
                 return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
             }
         };
-        auto mac = [&](int u, int g, double x0, double x1) {
-            const ulonglong2 a0 = ld_pair(c0 + 2 * g), a1 = ld_pair(c1 + 2 * g);
-            acc0[2 * u] = __dadd_rn(acc0[2 * u], mul_rt(from_u64(a0.x), x0, qinv, nq));
-            acc0[2 * u + 1] = __dadd_rn(acc0[2 * u + 1], mul_rt(from_u64(a0.y), x1, qinv, nq));
-            acc1[2 * u] = __dadd_rn(acc1[2 * u], mul_rt(from_u64(a1.x), x0, qinv, nq));
-            acc1[2 * u + 1] = __dadd_rn(acc1[2 * u + 1], mul_rt(from_u64(a1.y), x1, qinv, nq));
-        };
-        fwd_ntt<LGC>(buf, load, tw, nq, mac);
-        if (++since_red >= a.red_every) {
-            since_red = 0;
+        auto after_first = [&]() {  // mst consumed: fetch the next plaintext row
+            if (tid == 0 && d + 1 < d1) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&mbar, N * 4u);
 #pragma unroll
-            for (int e = 0; e < kE; ++e) {
-                acc0[e] = reduce(acc0[e], qinv, nq);
-                acc1[e] = reduce(acc1[e], qinv, nq);
+                for (int c = 0; c < 4; ++c)
+                    bulk_g2s(mst + c * (N / 4), Mb + (size_t)(d + 1) * N + c * (N / 4), N, &mbar);
             }
+        };
+        // model pairs of the last stage, two blocks (4 pairs each) ahead of their use
+        ulonglong2 mc[3][4];
+        auto load_block = [&](int c, ulonglong2 (&dst)[4]) {
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+                const int g = tid + (2 * c + uu) * NT;
+                dst[2 * uu] = ld_pair(c0 + 2 * g);
+                dst[2 * uu + 1] = ld_pair(c1 + 2 * g);
+            }
+        };
+        auto before_last = [&]() {
+            load_block(0, mc[0]);
+            load_block(1, mc[1]);
+        };
+        fwd_ntt_head<LGC>(buf, load, tw, nq, after_first, before_last);
+        // last stage + MAC, one 16-column TMEM block (two coefficient pairs) at a time
+        const bool red = ++since_red >= a.red_every;
+        if (red) since_red = 0;
+        ephdc_tmem::wait_st();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[16], t[8];
+            ephdc_tmem::ld16(tacc + 16 * c, r);
+            ephdc_tmem::ld8(ttw + 8 * c, t);
+            if (c + 2 < 4) load_block(c + 2, mc[(c + 2) % 3]);
+            ephdc_tmem::wait_ld(r);
+            ephdc_tmem::after_wait(t);
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+                double x0, x1;
+                fwd_ntt_tail<LGC>(buf, 2 * c + uu, __hiloint2double(t[4 * uu + 1], t[4 * uu]),
+                                  __hiloint2double(t[4 * uu + 3], t[4 * uu + 2]), nq, x0, x1);
+                const ulonglong2 m0v = mc[c % 3][2 * uu], m1v = mc[c % 3][2 * uu + 1];
+                uint32_t *w = &r[uu * 8];
+                double v[4] = {__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]),
+                               __hiloint2double(w[5], w[4]), __hiloint2double(w[7], w[6])};
+                v[0] = __dadd_rn(v[0], mul_rt(from_u64(m0v.x), x0, qinv, nq));
+                v[1] = __dadd_rn(v[1], mul_rt(from_u64(m0v.y), x1, qinv, nq));
+                v[2] = __dadd_rn(v[2], mul_rt(from_u64(m1v.x), x0, qinv, nq));
+                v[3] = __dadd_rn(v[3], mul_rt(from_u64(m1v.y), x1, qinv, nq));
+                if (red) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[e] = reduce(v[e], qinv, nq);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    w[2 * e] = (uint32_t)__double2loint(v[e]);
+                    w[2 * e + 1] = (uint32_t)__double2hiint(v[e]);
+                }
+            }
+            ephdc_tmem::st16(tacc + 16 * c, r);
         }
         __syncthreads();  // the next first pass overwrites buf
     }
     // fold this chunk's sum (canonical, < q) into the batch's scores ciphertext; the
     // sums of <= chunks values < q fit 64 bits (checked on the host) and integer
     // addition is order-independent, so the result is deterministic
-    u64 *o0 = out + (((size_t)b * 2 + 0) * a.L + j) * N + (size_t)s * NC;
-    u64 *o1 = out + (((size_t)b * 2 + 1) * a.L + j) * N + (size_t)s * NC;
+    {
+        uint32_t r[4][16];
+        ephdc_tmem::wait_st();
 #pragma unroll
-    for (int u = 0; u < kE / 2; ++u) {
-        const int g = tid + u * NT;
+        for (int c = 0; c < 4; ++c) ephdc_tmem::ld16(tacc + 16 * c, r[c]);
+        ephdc_tmem::wait_ld(r[0]);
+        ephdc_tmem::after_wait(r[1]);
+        ephdc_tmem::after_wait(r[2]);
+        ephdc_tmem::after_wait(r[3]);
+        u64 *o0 = out + (((size_t)b * 2 + 0) * a.L + j) * N + (size_t)s * NC;
+        u64 *o1 = out + (((size_t)b * 2 + 1) * a.L + j) * N + (size_t)s * NC;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const u64 v0 = to_canonical_u64(reduce(acc0[2 * u + e], qinv, nq), q);
-            const u64 v1 = to_canonical_u64(reduce(acc1[2 * u + e], qinv, nq), q);
-            atomicAdd(reinterpret_cast<unsigned long long *>(o0 + 2 * g + e), (unsigned long long)v0);
-            atomicAdd(reinterpret_cast<unsigned long long *>(o1 + 2 * g + e), (unsigned long long)v1);
+        for (int u = 0; u < kE / 2; ++u) {
+            const int g = tid + u * NT;
+            const uint32_t *w = &r[u >> 1][(u & 1) * 8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double v = reduce(__hiloint2double(w[2 * e + 1], w[2 * e]), qinv, nq);
+                u64 *o = (e < 2 ? o0 : o1) + 2 * g + (e & 1);
+                atomicAdd(reinterpret_cast<unsigned long long *>(o), (unsigned long long)to_canonical_u64(v, q));
+            }
         }
     }
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    if (warp == 0) ephdc_tmem::dealloc(tmem_slot, kCols);
 }
 
 // Plaintext NTTs for the parity export: p_hat[dd][j] = NTT_j(lift(M[dd])), canonical.
@@ -141,26 +255,20 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
 template <int LGC, int S>
 __global__ void EPHDC_F64_BOUNDS(LGC)
     k_pt_ntt_f64(const u32 *__restrict__ M, u64 *__restrict__ pt, F64MacArgs a) {
-    constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int NC = 1 << LGC, N = NC * S;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *tw = reinterpret_cast<double2 *>(smem_raw);
     double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * NC);
+    constexpr int NT = NC / kE;
     const int tid = threadIdx.x;
     u32 x = blockIdx.x;
     const u32 s = x % S;
     x /= S;
     const u32 j = x % a.L, dd = x / a.L;
     const double2 *twg = a.tw + (size_t)j * N;
-    const double2 qq = twg[0];  // slot 0 of the table holds (q_j, fl(1/q_j))
+    const double2 qq = twg[0];
     const double q = qq.x, nq = -q, qinv = qq.y;
-    for (int i = tid; i < NC; i += NT) {
-        if (i == 0) {
-            tw[0] = make_double2(0.0, 0.0);
-            continue;
-        }
-        const int m = 1 << (31 - __clz(i));
-        tw[i] = twg[S * m + (int)s * m + (i - m)];
-    }
+    load_twiddles<LGC, S>(tw, twg, (int)s, NC);
     double2 w1 = make_double2(0.0, 0.0);
     if constexpr (S > 1) w1 = twg[1];
     __syncthreads();
@@ -177,14 +285,20 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
             return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
         }
     };
+    auto none = [] {};
+    fwd_ntt_head<LGC>(buf, load, tw, nq, none, none);
     u64 *o = pt + ((size_t)dd * a.L + j) * N + (size_t)s * NC;
-    auto store = [&](int, int g, double x0, double x1) {
+#pragma unroll
+    for (int u = 0; u < kE / 2; ++u) {
+        const int g = tid + u * NT;
+        const double2 w = tw[NC / 2 + g];
+        double x0, x1;
+        fwd_ntt_tail<LGC>(buf, u, w.x, w.y, nq, x0, x1);
         ulonglong2 v;
         v.x = to_canonical_u64(reduce(x0, qinv, nq), q);
         v.y = to_canonical_u64(reduce(x1, qinv, nq), q);
         *reinterpret_cast<ulonglong2 *>(o + 2 * g) = v;
-    };
-    fwd_ntt<LGC>(buf, load, tw, nq, store);
+    }
 }
 
 // out[b][c][j][i] <- out mod q_j
@@ -221,13 +335,17 @@ template <class K> static cudaError_t smem_attr(K kernel, size_t bytes) {
 template <int LGC, int S>
 static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb, const u64 *model, u64 *out,
                                   cudaStream_t st) {
-    const size_t smem = ntt_f64_smem_bytes(LGC);
+    // pad shared memory so that no more CTAs share an SM than its TMEM holds
+    const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
     auto kern = k_ntt_mac_f64<LGC, S>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
     F64MacArgs a = f64_args(c);
     a.nb = nb;
     f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
+    // experiment knobs (profiling only; defaults are the tuned plan)
+    if (const char *e = getenv("EPHDC_F64_FLAGS")) a.flags = (u32)strtoul(e, nullptr, 0);
+    if (const char *e = getenv("EPHDC_F64_BG")) a.bg = std::max<u32>(1, std::min<u32>(nb, (u32)strtoul(e, nullptr, 0)));
     const uint64_t groups = (nb + a.bg - 1) / a.bg;
     const uint64_t grid = groups * a.chunks * a.bg * c->L * S;
     if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
@@ -281,9 +399,12 @@ cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, 
 }
 
 int ntt_mac_f64_occupancy(uint32_t log2N) {
-    const uint32_t lgc = log2N > 13 ? 13 : log2N;
-    const int occ = 8192 >> lgc;  // EPHDC_F64_BOUNDS; shared memory allows the same
-    return occ < 1 ? 1 : occ;
+    switch (log2N > 13 ? 13 : log2N) {
+        case 13: return f64_ctas_per_sm<13>();
+        case 12: return f64_ctas_per_sm<12>();
+        case 11: return f64_ctas_per_sm<11>();
+        default: return f64_ctas_per_sm<10>();
+    }
 }
 
 // Value bounds of the FP64 path: every input of

@@ -9,9 +9,14 @@
 // threads touch consecutive 16-byte pairs, i.e. the sink's global accesses coalesce.
 //
 // Twiddles: the CTA's slice of the bit-reversed psi table, (w, fl(w/q)) pairs, in
-// shared memory, indexed like the textbook loop (oracle/oracle_core.c): local stage
-// with m blocks uses tw[m + block].  A CTA owning slice s of S = N/NC (first global
-// stage done by the caller while loading) stores tw_global[S*m + s*m + block] there.
+// shared memory.  In the textbook loop (oracle/oracle_core.c) local stage with m
+// blocks uses psi_rev[m + block]; a CTA owning slice s of S = N/NC (first global stage
+// done by the caller while loading) needs psi_rev[S*m + s*m + block].  Inside a
+// radix-16 pass whose first stage has m0 blocks, sub-stage `sub` of block-group B uses
+// entries m0*2^sub + B*2^sub + v (v < 2^sub); the table stores that entry at slot
+// m0*2^sub + v*m0 + B so that the lanes of a warp (consecutive B) read consecutive
+// 16-byte slots -- free of shared-memory bank conflicts (the natural order has a
+// 2^sub * 16-byte lane stride, up to 16-way conflicts).
 #pragma once
 #include "modf64.cuh"
 
@@ -22,6 +27,7 @@ constexpr int padded_len(int n) { return n + n / 16; }
 constexpr int kE = 16;  // elements per thread
 
 // One pass of R = 2^R_LOG local stages with half-sizes 2^T0_LOG ... 2^(T0_LOG-R_LOG+1).
+// (LGC - 1 - T0_LOG is a multiple of 4: pass k starts at local stage level 4k.)
 template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
 EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double nq) {
     constexpr int R = 1 << R_LOG;
@@ -40,13 +46,13 @@ EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double n
             if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
             else x[k] = buf[pad(base + k * TL)];
         }
-        const int idx0 = ((1 << LGC) >> (T0_LOG + 1)) + blk;
+        constexpr int m0 = (1 << LGC) >> (T0_LOG + 1);
 #pragma unroll
         for (int sub = 0; sub < R_LOG; ++sub) {
             const int h = R >> (sub + 1);
 #pragma unroll
             for (int v = 0; v < (1 << sub); ++v) {
-                const double2 w = tw[(idx0 << sub) + v];
+                const double2 w = tw[(m0 << sub) + v * m0 + blk];
 #pragma unroll
                 for (int kk = 0; kk < h; ++kk) ct_bfly(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w.x, w.y, nq);
             }
@@ -57,34 +63,65 @@ EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double n
     __syncthreads();
 }
 
-// Stages with half-sizes 2^(REM-1) ... 2^1 in passes of <= 4; the first reads from load().
-template <int LGC, int REM, bool FIRST, class Load>
-EPHDC_D void fwd_passes(double *buf, const Load &load, const double2 *tw, double nq) {
+// Stages with half-sizes 2^(REM-1) ... 2^1 in passes of <= 4; the first reads from
+// load().  Hooks: before_last() runs before the last of these passes, after_first()
+// right after the first (behind its barrier: every thread has consumed load()).
+template <int LGC, int REM, bool FIRST, class Load, class H1, class H2>
+EPHDC_D void fwd_passes(double *buf, const Load &load, const double2 *tw, double nq, const H1 &after_first,
+                        const H2 &before_last) {
     if constexpr (REM > 1) {
         constexpr int R_LOG = (REM - 1) >= 4 ? 4 : (REM - 1);
+        if constexpr (REM - R_LOG <= 1) before_last();
         fwd_pass<LGC, REM - 1, R_LOG, FIRST>(buf, load, tw, nq);
-        fwd_passes<LGC, REM - R_LOG, false>(buf, load, tw, nq);
+        if constexpr (FIRST) after_first();
+        fwd_passes<LGC, REM - R_LOG, false>(buf, load, tw, nq, after_first, before_last);
     }
 }
 
-// Forward NTT of the NC = 2^LGC values load(i); the outputs of the last stage are
-// passed to sink(u, g, x0, x1) for the coefficient pairs (2g, 2g+1), g = tid + u*NT,
-// in the CTA's local bit-reversed evaluation order.  Values stay signed and lazy;
-// DESIGN.md gives their bounds.
-template <int LGC, class Load, class Sink>
-EPHDC_D void fwd_ntt(double *buf, const Load &load, const double2 *tw, double nq, const Sink &sink) {
-    static_assert(LGC >= 5, "at least one radix-16 pass before the final stage");
+// Fills tw_s[1..n_slots) (n_slots = NC/2: the head stages only, or NC: also the last
+// stage) with the slice-s twiddles of a prime (twg = [N] (w, w/q) pairs in psi_rev
+// order) in the pass layout described above.  All NT threads call it.
+template <int LGC, int S>
+EPHDC_D void load_twiddles(double2 *tw_s, const double2 *__restrict__ twg, int s, int n_slots) {
     constexpr int NT = (1 << LGC) / kE;
-    fwd_passes<LGC, LGC, true>(buf, load, tw, nq);
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int u = 0; u < kE / 2; ++u) {
-        const int g = tid + u * NT;
-        double x0 = buf[pad(2 * g)], x1 = buf[pad(2 * g + 1)];
-        const double2 w = tw[((1 << LGC) >> 1) + g];
-        ct_bfly(x0, x1, w.x, w.y, nq);
-        sink(u, g, x0, x1);
+    for (int p = threadIdx.x; p < n_slots; p += NT) {
+        if (p == 0) continue;
+        const int lm = 31 - __clz(p), m = 1 << lm;
+        int i = p;  // last stage (lm = LGC-1): natural order
+        if (lm < LGC - 1) {
+            const int start = lm & ~3, sub = lm - start, m0 = 1 << start;
+            const int r = p - m, v = r / m0, B = r % m0;
+            i = m + (B << sub) + v;
+        }
+        tw_s[p] = twg[S * m + s * m + (i - m)];
     }
+}
+
+// Global index (into a prime's psi_rev table) of the last-stage twiddle of pair g.
+template <int LGC, int S> EPHDC_D int tail_twiddle_index(int s, int g) {
+    constexpr int m = (1 << LGC) >> 1;
+    return S * m + s * m + g;
+}
+
+// All stages but the last (half-sizes NC/2 ... 2) of the forward NTT of the NC =
+// 2^LGC values load(i).  Values stay signed and lazy; DESIGN.md gives their bounds.
+template <int LGC, class Load, class H1, class H2>
+EPHDC_D void fwd_ntt_head(double *buf, const Load &load, const double2 *tw, double nq, const H1 &after_first,
+                          const H2 &before_last) {
+    static_assert(LGC >= 5, "at least one radix-16 pass before the final stage");
+    fwd_passes<LGC, LGC, true>(buf, load, tw, nq, after_first, before_last);
+}
+
+// Last stage (half-size 1) for the coefficient pair (2g, 2g+1), g = threadIdx.x + u*NT,
+// with its twiddle (w, w/q): consecutive threads own consecutive 16-byte pairs, so the
+// caller's global accesses coalesce.  Output order: the CTA's local bit-reversed order.
+template <int LGC>
+EPHDC_D void fwd_ntt_tail(const double *buf, int u, double w, double wq, double nq, double &x0, double &x1) {
+    constexpr int NT = (1 << LGC) / kE;
+    const int g = threadIdx.x + u * NT;
+    x0 = buf[pad(2 * g)];
+    x1 = buf[pad(2 * g + 1)];
+    ct_bfly(x0, x1, w, wq, nq);
 }
 
 }  // namespace ephdc_f64
