@@ -651,7 +651,7 @@ void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
 ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device, ephdc_ntt_plan **out) {
     if (!q || !out) return EPHDC_ENULL;
     *out = nullptr;
-    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 14) return EPHDC_EPARAM;
+    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16) return EPHDC_EPARAM;
     for (uint32_t j = 0; j < L; ++j)
         if (q[j] >= (1ull << 61) || !is_ntt_prime(q[j], log2N)) return EPHDC_EPARAM;
     if (device < 0) return EPHDC_ECONTEXT;

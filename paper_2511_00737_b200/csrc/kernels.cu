@@ -290,40 +290,102 @@ __global__ void __launch_bounds__((1 << LG) / kE)
 }
 
 // =====================================================================================
-// Standalone batched NTT (c5): CTA per (poly, prime), in place on [batch][L][N].
+// Standalone batched NTT (c5): CTA per (poly, prime, slice), in place on [batch][L][N].
+// N <= 2^14: one CTA holds the whole polynomial.  N = 2^15, 2^16: the first (forward)
+// or last (inverse) log2(N) - 14 stages run in k_ntt_global (one radix-2^GS butterfly
+// group per thread, straight from/to HBM) and S = N / 2^14 CTAs each transform one
+// slice of 2^14 coefficients in shared memory.
 // =====================================================================================
 struct NttArgs {
     PrimeSet ps;
     u32 L;
+    u32 log2N;               // full transform size (slices: LG < log2N)
     const TwPair<u64> *tw;   // [L][N]
     const u64 *ninv;         // [L][2]
 };
 
 template <int LG, bool INV>
 __global__ void __launch_bounds__((1 << LG) / kE) k_ntt_batch(u64 *__restrict__ polys, NttArgs a) {
-    constexpr int N = 1 << LG, NT = N / kE;
+    constexpr int NC = 1 << LG, NT = NC / kE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
-    const u32 j = blockIdx.x % a.L;
-    u64 *p = polys + (size_t)blockIdx.x * N;
+    const u32 S = 1u << (a.log2N - LG), N = 1u << a.log2N;
+    const u32 s = blockIdx.x % S, pj = blockIdx.x / S;   // pj = poly * L + j
+    const u32 j = pj % a.L;
+    u64 *p = polys + (size_t)pj * N + (size_t)s * NC;
     const u64 q = a.ps.q[j];
     const TwPair<u64> *tw = a.tw + (size_t)j * N;
     auto load = [&](int pos) -> u64 { return p[pos]; };
     if constexpr (!INV) {
-        fwd_ntt<u64, LG, kE>(buf, load, tw, (u32)N, q);
+        fwd_ntt<u64, LG, kE>(buf, load, tw, N + s * NC, q);
 #pragma unroll
         for (int e = 0; e < kE; ++e) {
             const int pos = threadIdx.x + e * NT;
             p[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
         }
     } else {
-        inv_ntt<u64, LG, kE>(buf, load, tw, q);
+        inv_ntt<u64, LG, kE>(buf, load, tw, q, N + s * NC);
+        if (S == 1) {
+            const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                const int pos = threadIdx.x + e * NT;
+                p[pos] = csub(mul_shoup_lazy<u64>(buf[pad(pos)], ni, nip, q), q);
+            }
+        } else {  // lazy [0, 2q): the global stages and N^-1 follow in k_ntt_global
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                const int pos = threadIdx.x + e * NT;
+                p[pos] = buf[pad(pos)];
+            }
+        }
+    }
+}
+
+// The GS = log2(N) - 14 global stages: forward (CT; first stages, canonical input ->
+// lazy [0, 4q)) or inverse (GS; last stages, lazy [0, 2q) input -> times N^-1,
+// canonical).  Thread = one radix-2^GS group {i + k * N/2^GS}.
+template <int GS, bool INV>
+__global__ void __launch_bounds__(256) k_ntt_global(u64 *__restrict__ polys, u32 n_polys, NttArgs a) {
+    constexpr int R = 1 << GS;
+    const u32 N = 1u << a.log2N, T = N >> GS;
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (size_t)n_polys * T) return;
+    const u32 pj = (u32)(gid / T), i = (u32)(gid % T), j = pj % a.L;
+    u64 *p = polys + (size_t)pj * N + i;
+    const u64 q = a.ps.q[j], two_q = 2 * q;
+    const TwPair<u64> *tw = a.tw + (size_t)j * N;
+    u64 x[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[k] = __ldcs(reinterpret_cast<const unsigned long long *>(p + (size_t)k * T));
+    if constexpr (!INV) {
+#pragma unroll
+        for (int sub = 0; sub < GS; ++sub) {
+            const int h = R >> (sub + 1);
+#pragma unroll
+            for (int v = 0; v < (1 << sub); ++v) {
+                const TwPair<u64> w = tw[(1 << sub) + v];
+#pragma unroll
+                for (int kk = 0; kk < h; ++kk) ct_bfly<u64>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w, q, two_q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) __stcs(reinterpret_cast<unsigned long long *>(p + (size_t)k * T), x[k]);
+    } else {
+#pragma unroll
+        for (int sub = 0; sub < GS; ++sub) {
+            const int hs = 1 << sub;
+#pragma unroll
+            for (int v = 0; v < R / (2 * hs); ++v) {
+                const TwPair<u64> w = tw[(R >> (sub + 1)) + v];
+#pragma unroll
+                for (int kk = 0; kk < hs; ++kk) gs_bfly<u64>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
+            }
+        }
         const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
 #pragma unroll
-        for (int e = 0; e < kE; ++e) {
-            const int pos = threadIdx.x + e * NT;
-            p[pos] = csub(mul_shoup_lazy<u64>(buf[pad(pos)], ni, nip, q), q);
-        }
+        for (int k = 0; k < R; ++k)
+            __stcs(reinterpret_cast<unsigned long long *>(p + (size_t)k * T), csub(mul_shoup_lazy<u64>(x[k], ni, nip, q), q));
     }
 }
 
@@ -548,11 +610,40 @@ static cudaError_t nttb_launch(const ephdc_ntt_plan *p, u64 *polys, u32 batch, c
     NttArgs a;
     a.ps = p->ps;
     a.L = p->L;
+    a.log2N = p->log2N;
     a.tw = INV ? p->itw : p->tw;
     a.ninv = p->ninv;
-    // grid.x limit is 2^31-1: batch * L fits
-    kern<<<batch * p->L, (1 << LG) / kE, smem, st>>>(polys, a);
+    const uint64_t grid = (uint64_t)batch * p->L << (p->log2N - LG);
+    if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+    kern<<<(unsigned)grid, (1 << LG) / kE, smem, st>>>(polys, a);
     return counted(cudaGetLastError());
+}
+
+template <int GS, bool INV>
+static cudaError_t nttg_launch(const ephdc_ntt_plan *p, u64 *polys, u32 batch, cudaStream_t st) {
+    NttArgs a;
+    a.ps = p->ps;
+    a.L = p->L;
+    a.log2N = p->log2N;
+    a.tw = INV ? p->itw : p->tw;
+    a.ninv = p->ninv;
+    const uint64_t n_polys = (uint64_t)batch * p->L;
+    const uint64_t threads = n_polys * (p->N >> GS);
+    const uint64_t blocks = (threads + 255) / 256;
+    if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+    k_ntt_global<GS, INV><<<(unsigned)blocks, 256, 0, st>>>(polys, (u32)n_polys, a);
+    return counted(cudaGetLastError());
+}
+
+template <bool INV>
+static cudaError_t ntt_large(const ephdc_ntt_plan *p, u64 *polys, u32 batch, cudaStream_t st) {
+    // forward: global stages, then 2^14-point slices; inverse: slices, then global stages
+    cudaError_t e = cudaSuccess;
+    if (!INV) e = p->log2N == 15 ? nttg_launch<1, false>(p, polys, batch, st) : nttg_launch<2, false>(p, polys, batch, st);
+    if (e != cudaSuccess) return e;
+    e = nttb_launch<14, INV>(p, polys, batch, st);
+    if (e != cudaSuccess || !INV) return e;
+    return p->log2N == 15 ? nttg_launch<1, true>(p, polys, batch, st) : nttg_launch<2, true>(p, polys, batch, st);
 }
 
 cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
@@ -566,6 +657,8 @@ cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_
         EPHDC_NTTB(12)
         EPHDC_NTTB(13)
         EPHDC_NTTB(14)
+        case 15:
+        case 16: return inverse ? ntt_large<true>(p, d_polys, batch, st) : ntt_large<false>(p, d_polys, batch, st);
     }
 #undef EPHDC_NTTB
     return cudaErrorInvalidValue;

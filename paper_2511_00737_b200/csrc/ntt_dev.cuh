@@ -80,7 +80,7 @@ EPHDC_D void fwd_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ tw,
 
 // One inverse pass: stages with half-sizes 2^T0_LOG ... 2^(T0_LOG+R_LOG-1).
 template <typename W, int LG, int E, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
-EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q, W two_q) {
+EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, u32 tw_num, W q, W two_q) {
     constexpr int R = 1 << R_LOG;
     constexpr int T0 = 1 << T0_LOG;
     constexpr int NT = (1 << LG) / E;
@@ -101,7 +101,7 @@ EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ it
             const int hs = 1 << sub;
 #pragma unroll
             for (int v = 0; v < R / (2 * hs); ++v) {
-                const u32 idx = ((u32)(1 << LG) >> (T0_LOG + sub + 1)) + (u32)((blk * R) >> (sub + 1)) + v;
+                const u32 idx = (tw_num >> (T0_LOG + sub + 1)) + (u32)((blk * R) >> (sub + 1)) + v;
                 const TwPair<W> w = itw[idx];
 #pragma unroll
                 for (int kk = 0; kk < hs; ++kk) gs_bfly<W>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
@@ -114,19 +114,21 @@ EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ it
 }
 
 template <typename W, int LG, int E, int DONE, bool FIRST, class Load>
-EPHDC_D void inv_passes(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q, W two_q) {
+EPHDC_D void inv_passes(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, u32 tw_num, W q, W two_q) {
     if constexpr (DONE < LG) {
         constexpr int R_LOG = (LG - DONE) >= 4 ? 4 : (LG - DONE);
-        inv_pass<W, LG, E, DONE, R_LOG, FIRST>(buf, load, itw, q, two_q);
-        inv_passes<W, LG, E, DONE + R_LOG, false>(buf, load, itw, q, two_q);
+        inv_pass<W, LG, E, DONE, R_LOG, FIRST>(buf, load, itw, tw_num, q, two_q);
+        inv_passes<W, LG, E, DONE + R_LOG, false>(buf, load, itw, tw_num, q, two_q);
     }
 }
 
 // Inverse NTT (without the final N^-1) of values from load(i) in [0, 2q);
-// result (lazy, [0, 2q)) in buf[pad(i)], natural coefficient order.
+// result (lazy, [0, 2q)) in buf[pad(i)], natural coefficient order.  As for the
+// forward transform, tw_num = N + s*NC makes a CTA that owns slice s of a larger
+// transform (the remaining global stages done by the caller) index global blocks.
 template <typename W, int LG, int E, class Load>
-EPHDC_D void inv_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q) {
-    inv_passes<W, LG, E, 0, true>(buf, load, itw, q, (W)(2 * q));
+EPHDC_D void inv_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, W q, u32 tw_num = 1u << LG) {
+    inv_passes<W, LG, E, 0, true>(buf, load, itw, tw_num, q, (W)(2 * q));
 }
 
 }  // namespace ephdc_ntt

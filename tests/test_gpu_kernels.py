@@ -23,7 +23,7 @@ def _host(t):
     return t.cpu().numpy().view(np.uint64)
 
 
-@pytest.mark.parametrize("log2N", [10, 12, 13, 14])
+@pytest.mark.parametrize("log2N", [10, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("L,bits", [(1, 30), (3, 60), (5, 60), (9, 48), (16, 30), (16, 60)])
 def test_ntt_fwd_inv_bitexact(log2N, L, bits):
     q = nt.prime_chain([bits] * L, log2N)
@@ -41,7 +41,8 @@ def test_ntt_fwd_inv_bitexact(log2N, L, bits):
     assert np.array_equal(_host(d), x)
 
 
-@pytest.mark.parametrize("log2N,L,bits,D", [(12, 3, 60, 5), (13, 5, 44, 64), (14, 9, 48, 33), (12, 16, 60, 300)])
+@pytest.mark.parametrize("log2N,L,bits,D", [(12, 3, 60, 5), (13, 5, 44, 64), (14, 9, 48, 33), (12, 16, 60, 300),
+                                            (15, 3, 60, 7), (16, 1, 30, 9), (16, 16, 60, 2)])
 def test_mac_bitexact(log2N, L, bits, D):
     N = 1 << log2N
     q = nt.prime_chain([bits] * L, log2N)
@@ -56,3 +57,26 @@ def test_mac_bitexact(log2N, L, bits, D):
             for d in range(D):
                 acc = (acc + ct[d, j, c].astype(object) * pt[d, j].astype(object)) % p
             assert np.array_equal(out[j, c], acc.astype(np.uint64)), (j, c)
+
+
+@pytest.mark.parametrize("log2N", [12, 13, 14, 15, 16])
+def test_ntt_c5_sampled_large_batch(log2N):
+    """BASELINE.json configs[4]: a larger batch, parity on the first, the last and
+    seeded-random polynomials (independent polynomials: the sample is sound)."""
+    N = 1 << log2N
+    L, bits = (9, 48) if log2N <= 14 else (5, 60)
+    q = nt.prime_chain([bits] * L, log2N)
+    batch = max(1, (1 << 22) // (N * L))            # ~32 MB of residues
+    x = inp.gen_residues(q, batch, N, seed=4242 + log2N)
+    plan = eph.NttPlan(q, log2N)
+    d = _dev(x)
+    eph.ntt_fwd(plan, d)
+    got = _host(d)
+    rng = np.random.default_rng(log2N)
+    picks = sorted({0, batch - 1, *rng.integers(0, batch, 6).tolist()})
+    for b in picks:
+        for j, p in enumerate(q):
+            psi = nt.min_primitive_2n_root(p, N)
+            assert np.array_equal(got[b, j], core.ntt_fwd(x[b, j][None, :], log2N, p, psi)[0]), (b, j)
+    eph.ntt_inv(plan, d)
+    assert np.array_equal(_host(d), x)
