@@ -184,13 +184,15 @@ def main():
     import torch.distributed as dist
     import paper_2511_00737_b200 as eph
     from paper_2511_00737_b200 import pipeline as ppipe
+    from paper_2511_00737_b200 import dist as pdist
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    Xtr, ytr, Xq, _ = inp.gen_features(cfg)
+    # every rank: the same model (replicated), its own query stream (weak scaling)
+    Xtr, ytr, Xq, _ = inp.gen_features(cfg, stream=rank)
     P = inp.gen_projection(cfg)
     ps = ppipe.build(cfg, P, Xtr, ytr, device=local)
     ctx, model = ps.ctx, ps.model
@@ -236,10 +238,7 @@ def main():
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = pdist.max_over_ranks(ms)
     value = world * nq / (ms_max / 1e3)
 
     # roofline of the dominant kernel: the fused lift + NTT_q + MAC (all batches per launch)
@@ -295,10 +294,8 @@ def main():
             eph.classify_host(ctx, model, ws, Xh, ps.P_dev, oh)
         f1.record(stream)
         torch.cuda.synchronize(dev)
-        ems = torch.tensor([f0.elapsed_time(f1) / a.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * nq / (float(ems.item()) / 1e3), "unit": "queries/s",
+        ems = pdist.max_over_ranks(f0.elapsed_time(f1) / a.steps)
+        e2e = {"value": world * nq / (ems / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": int(Xh.numel()), "d2h_bytes_per_step": int(oh.numel() * 8)}
 
     cpu = None

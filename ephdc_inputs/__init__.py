@@ -91,11 +91,13 @@ def _clip_range(cfg: Config) -> Tuple[int, int]:
     return (0, 255) if cfg.feat_unsigned else (-128, 127)
 
 
-def gen_features(cfg: Config, nq: Optional[int] = None):
+def gen_features(cfg: Config, nq: Optional[int] = None, stream: int = 0):
     """Returns (X_train, y_train, X_query, y_query).
 
     X_* are uint8 (c3) or int8 row-major [n, F]; y_* int64 class labels.
-    Query i is drawn from cluster i mod k.
+    Query i is drawn from cluster i mod k.  stream > 0 draws an independent query set
+    (seed (cfg.seed, stream)) from the same clusters and training set: the per-rank
+    query streams of a multi-GPU run.
     """
     nq = cfg.nq if nq is None else nq
     rng = np.random.default_rng(cfg.seed)
@@ -103,15 +105,15 @@ def gen_features(cfg: Config, nq: Optional[int] = None):
     lo, hi = _clip_range(cfg)
     dt = np.uint8 if cfg.feat_unsigned else np.int8
 
-    def draw(labels: np.ndarray) -> np.ndarray:
-        z = rng.standard_normal(size=(labels.size, cfg.F))
+    def draw(labels: np.ndarray, g) -> np.ndarray:
+        z = g.standard_normal(size=(labels.size, cfg.F))
         x = np.clip(np.rint(mu[labels] + cfg.sigma * z), lo, hi)
         return x.astype(dt)
 
     y_train = np.repeat(np.arange(cfg.k, dtype=np.int64), cfg.n_train_per_class)
-    X_train = draw(y_train)
+    X_train = draw(y_train, rng)
     y_query = np.arange(nq, dtype=np.int64) % cfg.k
-    X_query = draw(y_query)
+    X_query = draw(y_query, rng if stream == 0 else np.random.default_rng([cfg.seed, stream]))
     return X_train, y_train, X_query, y_query
 
 
