@@ -32,7 +32,6 @@ def main():
     import torch
     import ephdc_inputs as inp
     import paper_2511_00737_b200 as eph
-    from oracle import nt  # prime chains only (host number theory, not the kernels)
 
     peaks = {}
     try:
@@ -47,7 +46,7 @@ def main():
     dev = torch.device("cuda", 0)
     for lg, L, bits in pts:
         N = 1 << lg
-        q = nt.prime_chain([bits] * L, lg)
+        q = eph.find_ntt_primes(lg, [bits] * L)
         plan = eph.NttPlan(q, lg)
         per_poly = L * N * 8
         batch = max(1, int(a.bytes * (1 << 30) // per_poly))
