@@ -359,6 +359,8 @@ ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const i
         EPHDC_CUDA_TRY(launch_pack_intt_model(c, (const int8_t *)bC.p, d0, nd, (uint32_t *)bM.p, st));
         EPHDC_CUDA_TRY(launch_encrypt(c, (const uint32_t *)bM.p, d0, nd, (const uint64_t *)bS.p, seed, m->d_ct, st));
     }
+    // FP64 path: keep the residues as exact doubles (the fused kernel's operand format)
+    if (c->f64.enabled) EPHDC_CUDA_TRY(launch_u64_to_f64(m->d_ct, (size_t)D * L * 2 * N, st));
     EPHDC_CUDA_TRY(cudaDeviceSynchronize());
     *out = m.release();
     return EPHDC_OK;
@@ -371,6 +373,13 @@ ephdc_status ephdc_model_export(const ephdc_model *m, uint32_t d0, uint32_t nd, 
     const size_t per = (size_t)c->L * 2 * c->N;
     EPHDC_CUDA_TRY(cudaSetDevice(c->device));
     EPHDC_CUDA_TRY(cudaMemcpy(host_out, m->d_ct + per * d0, sizeof(uint64_t) * per * nd, cudaMemcpyDeviceToHost));
+    if (c->f64.enabled) {  // stored as exact doubles < 2^50: back to canonical u64
+        for (size_t i = 0; i < per * nd; ++i) {
+            double v;
+            memcpy(&v, &host_out[i], sizeof v);
+            host_out[i] = (uint64_t)v;
+        }
+    }
     return EPHDC_OK;
 }
 
@@ -496,7 +505,7 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
             }
             {
                 Timer tm(ws, st, kClsMac);
-                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->d_M, g, m->d_ct, d_out + per * b0, st));
+                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->d_M, g, reinterpret_cast<const double *>(m->d_ct), d_out + per * b0, st));
                 tm.done();
             }
         }

@@ -81,14 +81,14 @@ struct ephdc_sk {
 
 struct ephdc_model {
     const ephdc_ctx *ctx = nullptr;
-    uint64_t *d_ct = nullptr;     // [D_live][L][2][N]
+    uint64_t *d_ct = nullptr;     // [D_live][L][2][N]: u64 (integer path) or exact doubles (FP64 path)
     uint32_t D = 0;
 };
 
 struct ephdc_workspace {
     const ephdc_ctx *ctx = nullptr;
     uint32_t max_nq = 0;
-    uint32_t *d_M = nullptr;      // [m_batches][D_live][N] encoded plaintexts (mod t)
+    uint32_t *d_M = nullptr;      // [m_batches][D_live][N] encoded plaintexts, centered int32 (#3)
     uint32_t m_batches = 1;       // batches d_M holds (FP64 path: all of max_nq, capped)
     void *d_X = nullptr;          // [max_nq][F]
     int8_t *d_H = nullptr;        // [D_live][max_nq]
@@ -138,8 +138,9 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
                        uint64_t *d_out, cudaStream_t st);
 size_t ntt_mac_smem_bytes(uint32_t log2Nc);
 // FP64-pipe path (kernels_f64.cu)
-cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const uint64_t *d_model,
+cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
                                uint64_t *d_out, cudaStream_t st);
+cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st);
 cudaError_t launch_plaintext_ntt_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
                                      cudaStream_t st);
 cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, cudaStream_t st);

@@ -134,11 +134,15 @@ __global__ void __launch_bounds__((1 << LG) / kE)
     };
     inv_ntt<u32, LG, kE>(buf, load, a.itw, t);
     u32 *out = M + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * N;
+    const u32 half_t = (t - 1) / 2;
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
         const int pos = threadIdx.x + e * NT;
-        u32 y = mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t);
-        out[pos] = csub(y, t);
+        const u32 y = csub(mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t), t);
+        // model plaintexts stay in [0, t) (Delta * m, reading #4); query plaintexts are
+        // stored as their centered lift (reading #3), a signed int32 (|m| < t/2 < 2^29)
+        if constexpr (MODEL) out[pos] = y;
+        else out[pos] = y <= half_t ? y : (u32)((int)y - (int)t);
     }
 }
 
@@ -164,17 +168,16 @@ __global__ void __launch_bounds__((1 << LGC) / kE)
     const u32 x = blockIdx.x;
     const u32 js = x % (a.L * S), chunk = x / (a.L * S);
     const u32 j = js / S, s = js % S;
-    const u64 q = a.ps.q[j], qinv = a.ps.qinv[j], two_q = 2 * q, qmt = a.ps.qmt[j];
+    const u64 q = a.ps.q[j], qinv = a.ps.qinv[j], two_q = 2 * q;
     const TwPair<u64> *tw = a.tw + (size_t)j * N;
     const u32 d0 = chunk * a.G, d1 = min(a.D_live, d0 + a.G);
 #pragma unroll
     for (int e = 0; e < 2 * kE; ++e) acc[e * NT + tid] = 0;
     TwPair<u64> w1{0, 0};
     if constexpr (S > 1) w1 = tw[1];
-    const u32 half_t = a.half_t;
     for (u32 d = d0; d < d1; ++d) {
         const u32 *m = M + (size_t)d * N;
-        auto lift = [&](u32 v) -> u64 { return v <= half_t ? (u64)v : (u64)v + qmt; };
+        auto lift = [&](u32 v) -> u64 { return (int)v >= 0 ? (u64)v : (u64)(int64_t)(int)v + q; };
         auto load = [&](int pos) -> u64 {
             const u64 U = lift(__ldg(m + pos));
             if constexpr (S == 1) {
@@ -227,12 +230,11 @@ __global__ void __launch_bounds__((1 << LG) / kE)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
     const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L;
-    const u64 q = a.ps.q[j], qmt = a.ps.qmt[j];
+    const u64 q = a.ps.q[j];
     const u32 *m = M + (size_t)dd * N;
-    const u32 half_t = a.half_t;
     auto load = [&](int pos) -> u64 {
         const u32 v = m[pos];
-        return v <= half_t ? (u64)v : (u64)v + qmt;
+        return (int)v >= 0 ? (u64)v : (u64)(int64_t)(int)v + q;
     };
     fwd_ntt<u64, LG, kE>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
     u64 *o = pt + ((size_t)dd * a.L + j) * N;

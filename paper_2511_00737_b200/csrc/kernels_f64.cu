@@ -29,7 +29,7 @@ namespace {
 
 EPHDC_D void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-EPHDC_D ulonglong2 ld_pair(const u64 *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
+EPHDC_D double2 ld_pair(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
 
 inline cudaError_t counted(cudaError_t e) {
     if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -63,7 +63,7 @@ template <int LGC, int S> constexpr size_t mac_f64_smem() {
 
 template <int LGC, int S>
 __global__ void EPHDC_F64_BOUNDS(LGC)
-    k_ntt_mac_f64(const u32 *__restrict__ M, const u64 *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
+    k_ntt_mac_f64(const u32 *__restrict__ M, const double *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
     using namespace ephdc_async;
     constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
     constexpr uint32_t kCols = tmem_cols<LGC>();
@@ -132,12 +132,10 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         }
     }
 
-    const u32 half_t = a.half_t;
-    const double two52t = a.two52_plus_t;
     u32 since_red = 0, phase = 0;
     for (u32 d = d0; d < d1; ++d) {
-        const u64 *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
-        const u64 *c1 = c0 + N;
+        const double *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
+        const double *c1 = c0 + N;
         if (!(a.flags & 1u)) {
             prefetch_l2(c0 + 16 * tid);  // this dim's model slice, read by the last stage
             prefetch_l2(c1 + 16 * tid);
@@ -145,12 +143,12 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         mbar_wait(&mbar, phase);     // plaintext row d is in mst
         phase ^= 1u;
         auto load = [&](int pos) -> double {
-            const double U = lift_centered(mst[pos], half_t, two52t);
+            const double U = from_i32((int)mst[pos]);
             if constexpr (S == 1) {
                 return U;
             } else {
                 // first global stage (half-size N/2) fused into the load: slice s keeps U +- w V
-                const double V = lift_centered(mst[pos + NC], half_t, two52t);
+                const double V = from_i32((int)mst[pos + NC]);
                 const double T = mul_tw(V, w1.x, w1.y, nq);
                 return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
             }
@@ -164,9 +162,10 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
                     bulk_g2s(mst + c * (N / 4), Mb + (size_t)(d + 1) * N + c * (N / 4), N, &mbar);
             }
         };
-        // model pairs of the last stage, two blocks (4 pairs each) ahead of their use
-        ulonglong2 mc[3][4];
-        auto load_block = [&](int c, ulonglong2 (&dst)[4]) {
+        // model pairs of the last stage: blocks 0, 1 (4 pairs each) are requested before the
+        // last head pass, blocks 2, 3 when the last stage starts
+        double2 mc[4][4];
+        auto load_block = [&](int c, double2 (&dst)[4]) {
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
                 const int g = tid + (2 * c + uu) * NT;
@@ -183,12 +182,13 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         const bool red = ++since_red >= a.red_every;
         if (red) since_red = 0;
         ephdc_tmem::wait_st();
+        load_block(2, mc[2]);
+        load_block(3, mc[3]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t r[16], t[8];
             ephdc_tmem::ld16(tacc + 16 * c, r);
             ephdc_tmem::ld8(ttw + 8 * c, t);
-            if (c + 2 < 4) load_block(c + 2, mc[(c + 2) % 3]);
             ephdc_tmem::wait_ld(r);
             ephdc_tmem::after_wait(t);
 #pragma unroll
@@ -196,14 +196,14 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
                 double x0, x1;
                 fwd_ntt_tail<LGC>(buf, 2 * c + uu, __hiloint2double(t[4 * uu + 1], t[4 * uu]),
                                   __hiloint2double(t[4 * uu + 3], t[4 * uu + 2]), nq, x0, x1);
-                const ulonglong2 m0v = mc[c % 3][2 * uu], m1v = mc[c % 3][2 * uu + 1];
+                const double2 m0v = mc[c][2 * uu], m1v = mc[c][2 * uu + 1];
                 uint32_t *w = &r[uu * 8];
                 double v[4] = {__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]),
                                __hiloint2double(w[5], w[4]), __hiloint2double(w[7], w[6])};
-                v[0] = __dadd_rn(v[0], mul_rt(from_u64(m0v.x), x0, qinv, nq));
-                v[1] = __dadd_rn(v[1], mul_rt(from_u64(m0v.y), x1, qinv, nq));
-                v[2] = __dadd_rn(v[2], mul_rt(from_u64(m1v.x), x0, qinv, nq));
-                v[3] = __dadd_rn(v[3], mul_rt(from_u64(m1v.y), x1, qinv, nq));
+                v[0] = __dadd_rn(v[0], mul_rt(m0v.x, x0, qinv, nq));
+                v[1] = __dadd_rn(v[1], mul_rt(m0v.y, x1, qinv, nq));
+                v[2] = __dadd_rn(v[2], mul_rt(m1v.x, x0, qinv, nq));
+                v[3] = __dadd_rn(v[3], mul_rt(m1v.y, x1, qinv, nq));
                 if (red) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) v[e] = reduce(v[e], qinv, nq);
@@ -273,14 +273,12 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     if constexpr (S > 1) w1 = twg[1];
     __syncthreads();
     const u32 *m = M + (size_t)dd * N;
-    const u32 half_t = a.half_t;
-    const double two52t = a.two52_plus_t;
     auto load = [&](int pos) -> double {
-        const double U = lift_centered(m[pos], half_t, two52t);
+        const double U = from_i32((int)m[pos]);
         if constexpr (S == 1) {
             return U;
         } else {
-            const double V = lift_centered(m[pos + NC], half_t, two52t);
+            const double V = from_i32((int)m[pos + NC]);
             const double T = mul_tw(V, w1.x, w1.y, nq);
             return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
         }
@@ -299,6 +297,18 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         v.y = to_canonical_u64(reduce(x1, qinv, nq), q);
         *reinterpret_cast<ulonglong2 *>(o + 2 * g) = v;
     }
+}
+
+// model residues u64 -> exact doubles, in place (setup, once per model)
+__global__ void k_u64_to_f64(u64 *__restrict__ d, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = (u64)__double_as_longlong(from_u64(d[i]));
+}
+
+cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_u64_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d, n);
+    return counted(cudaGetLastError());
 }
 
 // out[b][c][j][i] <- out mod q_j
@@ -333,7 +343,7 @@ template <class K> static cudaError_t smem_attr(K kernel, size_t bytes) {
 }
 
 template <int LGC, int S>
-static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb, const u64 *model, u64 *out,
+static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb, const double *model, u64 *out,
                                   cudaStream_t st) {
     // pad shared memory so that no more CTAs share an SM than its TMEM holds
     const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
@@ -354,7 +364,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
 }
 
 
-cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const uint64_t *d_model,
+cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
                                uint64_t *d_out, cudaStream_t st) {
     if (nb == 0) return cudaSuccess;
     switch (c->p.log2N) {

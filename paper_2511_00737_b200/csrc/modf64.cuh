@@ -75,10 +75,9 @@ EPHDC_D void gs_bfly(double &X, double &Y, double w, double wq, double nq) {
 EPHDC_D double from_u64(uint64_t v) {  // v < 2^52
     return __dsub_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), kTwo52);
 }
-// u32 residue m in [0, t) -> centered representative (m > half ? m - t : m) (reading #3)
-EPHDC_D double lift_centered(uint32_t m, uint32_t half_t, double two52_plus_t) {
-    const double big = __hiloint2double(0x43300000, (int)m);  // 2^52 + m
-    return __dsub_rn(big, m > half_t ? two52_plus_t : kTwo52);
+// signed int32 v -> double, exact: the bit pattern 0x43300000:(v ^ 2^31) is 2^52 + 2^31 + v
+EPHDC_D double from_i32(int v) {
+    return __dsub_rn(__hiloint2double(0x43300000, v ^ (int)0x80000000), 4503601774854144.0);
 }
 // canonical residue: r in (-q, q) -> [0, q) as u64
 EPHDC_D uint64_t to_canonical_u64(double r, double q) {
