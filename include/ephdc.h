@@ -77,7 +77,14 @@ typedef struct {
                               * EPHDC_ARITH_INT (1): integer pipe (u64 Shoup/Montgomery);
                               * EPHDC_ARITH_F64 (2): FP64 pipe, EPARAM if not eligible.
                               * Both give bit-identical results.                    */
+    uint32_t encoder;        /* HDC encoding GEMM: EPHDC_ENCODER_AUTO (0): tcgen05
+                              * kind::i8 tensor-core kernel fed by TMA when F % 16 == 0
+                              * (else CUDA-core dp4a); EPHDC_ENCODER_DP4A (1): dp4a.
+                              * Both are exact (int32).                              */
 } ephdc_params;
+
+#define EPHDC_ENCODER_AUTO 0u
+#define EPHDC_ENCODER_DP4A 1u
 
 #define EPHDC_ARITH_AUTO 0u
 #define EPHDC_ARITH_INT 1u

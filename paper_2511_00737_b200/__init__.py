@@ -73,10 +73,11 @@ class Context:
 
     def __init__(self, *, log2N: int, q: Sequence[int], t: int, k: int, D_live: int, D_stored: int, F: int,
                  feat_unsigned: bool, Qbits: int, Cbits: int, qshift: int, sigma_e: float = 3.2,
-                 device: int = 0, arith: int = 0):
+                 device: int = 0, arith: int = 0, encoder: int = 0):
         self._q = np.ascontiguousarray(np.array(q, dtype=np.uint64))
         self.params = _capi.Params(log2N, len(q), self._q.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), t, k,
-                                   D_live, D_stored, F, int(feat_unsigned), Qbits, Cbits, qshift, sigma_e, arith)
+                                   D_live, D_stored, F, int(feat_unsigned), Qbits, Cbits, qshift, sigma_e, arith,
+                                   encoder)
         self._h = ctypes.c_void_p()
         call("ephdc_ctx_create", ctypes.byref(self.params), device, ctypes.byref(self._h))
         info = _capi.CtxInfo()

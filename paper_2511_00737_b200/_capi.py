@@ -32,7 +32,7 @@ class Params(ctypes.Structure):
         ("log2N", c_u32), ("L", c_u32), ("q", ctypes.POINTER(c_u64)), ("t", c_u64),
         ("k", c_u32), ("D_live", c_u32), ("D_stored", c_u32), ("F", c_u32),
         ("feat_unsigned", c_u32), ("Qbits", c_u32), ("Cbits", c_u32), ("qshift", c_u32),
-        ("sigma_e", ctypes.c_double), ("arith", c_u32),
+        ("sigma_e", ctypes.c_double), ("arith", c_u32), ("encoder", c_u32),
     ]
 
 

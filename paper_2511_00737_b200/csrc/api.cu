@@ -209,7 +209,7 @@ ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out
         c->fused_G = (uint32_t)((p->D_live + chunks - 1) / chunks);
         c->fused_chunks = (p->D_live + c->fused_G - 1) / c->fused_G;
     }
-    if (p->arith > EPHDC_ARITH_F64) return EPHDC_EPARAM;
+    if (p->arith > EPHDC_ARITH_F64 || p->encoder > EPHDC_ENCODER_DP4A) return EPHDC_EPARAM;
     if (p->arith != EPHDC_ARITH_INT) {
         const bool ok = plan_f64(c->q, p->t, p->log2N, &c->f64);
         if (!ok && p->arith == EPHDC_ARITH_F64) return EPHDC_EPARAM;

@@ -137,6 +137,10 @@ cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_
 cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
                        uint64_t *d_out, cudaStream_t st);
 size_t ntt_mac_smem_bytes(uint32_t log2Nc);
+// tcgen05 int8 encoder (encode_tc.cu)
+bool encode_tc_supported(const ephdc_ctx *c);
+cudaError_t launch_encode_tc(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, void *d_H, bool raw,
+                             cudaStream_t st);
 // FP64-pipe path (kernels_f64.cu)
 cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
                                uint64_t *d_out, cudaStream_t st);

@@ -433,6 +433,13 @@ static inline cudaError_t counted(cudaError_t e, uint64_t n = 1) {
 
 cudaError_t launch_encode(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, void *d_H, bool raw,
                           cudaStream_t st) {
+    // tensor-core path (encode_tc.cu) unless disabled or unsupported (F % 16 != 0,
+    // operands not 16-byte aligned for TMA)
+    if (c->p.encoder != EPHDC_ENCODER_DP4A && encode_tc_supported(c) && ((uintptr_t)d_X & 15) == 0 &&
+        ((uintptr_t)d_P & 15) == 0) {
+        cudaError_t e = launch_encode_tc(c, d_X, d_P, nq, d_H, raw, st);
+        if (e != cudaErrorInvalidValue) return e;
+    }
     dim3 grid((nq + 63) / 64, (c->p.D_live + 63) / 64);
     const int qmax = (1 << (c->p.Qbits - 1)) - 1;
     const uint8_t *X = (const uint8_t *)d_X;

@@ -40,28 +40,31 @@ def primes_for(cfg: inp.Config):
     return t, q
 
 
-def make_context(cfg: inp.Config, t: int, q, Qbits: int, qshift: int, device: int = 0, arith: int = 0) -> Context:
+def make_context(cfg: inp.Config, t: int, q, Qbits: int, qshift: int, device: int = 0, arith: int = 0,
+                 encoder: int = 0) -> Context:
     return Context(log2N=cfg.log2N, q=q, t=t, k=cfg.k, D_live=cfg.D_live, D_stored=cfg.D_stored, F=cfg.F,
                    feat_unsigned=cfg.feat_unsigned, Qbits=Qbits, Cbits=cfg.Cbits, qshift=qshift,
-                   sigma_e=cfg.sigma_e, device=device, arith=arith)
+                   sigma_e=cfg.sigma_e, device=device, arith=arith, encoder=encoder)
 
 
 def build(cfg: inp.Config, P: np.ndarray, X_train: np.ndarray, y_train: np.ndarray, device: int = 0,
-          sk_seed: Optional[int] = None, enc_seed: Optional[int] = None, arith: int = 0) -> Setup:
-    """arith: 0 auto (FP64 pipe when eligible), 1 integer pipe, 2 FP64 pipe (ephdc_params.arith)."""
+          sk_seed: Optional[int] = None, enc_seed: Optional[int] = None, arith: int = 0,
+          encoder: int = 0) -> Setup:
+    """arith: 0 auto (FP64 pipe when eligible), 1 integer pipe, 2 FP64 pipe (ephdc_params.arith);
+    encoder: 0 auto (tcgen05 tensor cores), 1 dp4a CUDA cores (ephdc_params.encoder)."""
     import torch
     dev = torch.device("cuda", device)
     t, q = primes_for(cfg)
     Qbits = model_build.query_bits(cfg.D_live, cfg.Cbits, t)
     P_dev = torch.from_numpy(np.ascontiguousarray(P)).to(dev)
     # training projection on the GPU (the quantisation fields are unused by encode_raw)
-    ctx0 = make_context(cfg, t, q, Qbits, 0, device)
+    ctx0 = make_context(cfg, t, q, Qbits, 0, device, arith, encoder)
     Xt = torch.from_numpy(np.ascontiguousarray(X_train).view(np.int8)).to(dev)
     acc = encode_raw(ctx0, Xt, P_dev).cpu().numpy()
     torch.cuda.synchronize(dev)
     class_hv, qshift = model_build.train(acc, y_train, cfg.k, cfg.Cbits, Qbits)
     ctx0.close()
-    ctx = make_context(cfg, t, q, Qbits, qshift, device, arith)
+    ctx = make_context(cfg, t, q, Qbits, qshift, device, arith, encoder)
     sk = SecretKey(ctx, cfg.seed + SK_SEED_OFFSET if sk_seed is None else sk_seed)
     model = EncryptedModel(ctx, sk, class_hv, cfg.seed + ENC_SEED_OFFSET if enc_seed is None else enc_seed)
     return Setup(cfg, ctx, sk, model, class_hv, P_dev, Qbits, qshift)
