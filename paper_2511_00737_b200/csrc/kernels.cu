@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "internal.h"
 #include "ntt_dev.cuh"
@@ -143,6 +144,108 @@ __global__ void __launch_bounds__((1 << LG) / kE)
         // stored as their centered lift (reading #3), a signed int32 (|m| < t/2 < 2^29)
         if constexpr (MODEL) out[pos] = y;
         else out[pos] = y <= half_t ? y : (u32)((int)y - (int)t);
+    }
+}
+
+// Inverse (Gentleman-Sande) passes over a twiddle table held in shared memory in the
+// pass-major layout: the twiddle of (sub-stage sub, block-group blk, v) sits at slot
+// N/2^(T0+sub+1) + v*nblk + blk, so a warp's lanes (consecutive blk) read consecutive
+// pairs.  Same arithmetic as ntt_dev.cuh inv_pass (u32, lazy [0, 2t)).
+// one Gentleman-Sande sub-stage (compile-time trip counts, so x[] stays in registers)
+template <int N_, int T0_LOG, int R_LOG, int SUB>
+EPHDC_D void gs_substages(u32 (&x)[1 << R_LOG], const TwPair<u32> *tw, int blk, u32 t, u32 two_t) {
+    if constexpr (SUB < R_LOG) {
+        constexpr int R = 1 << R_LOG, hs = 1 << SUB, nv = R / (2 * hs), nblk = N_ >> (T0_LOG + R_LOG);
+#pragma unroll
+        for (int v = 0; v < nv; ++v) {
+            const TwPair<u32> w = tw[(N_ >> (T0_LOG + SUB + 1)) + v * nblk + blk];
+#pragma unroll
+            for (int kk = 0; kk < hs; ++kk) gs_bfly<u32>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, t, two_t);
+        }
+        gs_substages<N_, T0_LOG, R_LOG, SUB + 1>(x, tw, blk, t, two_t);
+    }
+}
+
+template <int LG, int T0_LOG, int R_LOG, bool FIRST, class Load>
+EPHDC_D void inv_pass_perm(u32 *buf, const Load &load, const TwPair<u32> *tw, u32 t, u32 two_t) {
+    constexpr int N = 1 << LG, NT = N / kE;
+    constexpr int R = 1 << R_LOG, T0 = 1 << T0_LOG;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kE / R; ++u) {
+        const int g = tid + u * NT;
+        const int blk = g >> T0_LOG, off = g & (T0 - 1);
+        const int base = blk * (T0 * R) + off;
+        u32 x[R];
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk) {
+            if constexpr (FIRST) x[kk] = load(base + kk * T0);
+            else x[kk] = buf[pad(base + kk * T0)];
+        }
+        gs_substages<N, T0_LOG, R_LOG, 0>(x, tw, blk, t, two_t);
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk) buf[pad(base + kk * T0)] = x[kk];
+    }
+    __syncthreads();
+}
+
+template <int LG, int DONE, bool FIRST, class Load>
+EPHDC_D void inv_passes_perm(u32 *buf, const Load &load, const TwPair<u32> *tw, u32 t, u32 two_t) {
+    if constexpr (DONE < LG) {
+        constexpr int R_LOG = (LG - DONE) >= 4 ? 4 : (LG - DONE);
+        inv_pass_perm<LG, DONE, R_LOG, FIRST>(buf, load, tw, t, two_t);
+        inv_passes_perm<LG, DONE + R_LOG, false>(buf, load, tw, t, two_t);
+    }
+}
+
+// =====================================================================================
+// K2 (query path, persistent): slot pack + INTT mod t for a range of (batch, dim) rows.
+// A CTA keeps the whole psi_t^-1 table in shared memory in the pass-major layout (the
+// lanes of a warp read consecutive 8-byte pairs: conflict-free) and loops over rows
+// with stride gridDim.x; the slot -> query division i / k is a multiply-high by
+// m = floor(2^32 / k) + 1 (exact for i < 2^16, k <= 2^16).  Output: centered int32.
+// =====================================================================================
+template <int LG>
+__global__ void __launch_bounds__((1 << LG) / kE, (LG >= 14) ? 1 : (16384 >> LG))
+    k_pack_intt_q(const int8_t *__restrict__ H, u32 nq, u32 b0, u32 nbat, u32 D, PackArgs a, u32 kmagic,
+                  u32 *__restrict__ M) {
+    constexpr int N = 1 << LG, NT = N / kE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TwPair<u32> *tw = reinterpret_cast<TwPair<u32> *>(smem_raw);         // [N]
+    u32 *buf = reinterpret_cast<u32 *>(smem_raw + sizeof(TwPair<u32>) * N);
+    const int tid = threadIdx.x;
+    for (int p = tid; p < N; p += NT) {
+        if (p == 0) continue;
+        const int lsb = 31 - __clz(p), sb = 1 << lsb;       // stage with sb blocks, half-size N/(2 sb)
+        const int st = LG - 1 - lsb;                        // log2 of the half-size
+        const int done = st & ~3, sub = st - done;
+        const int rlog = (LG - done) < 4 ? (LG - done) : 4;
+        const int nblk = N >> (done + rlog);
+        const int r = p - sb, v = r / nblk, blk = r % nblk;
+        tw[p] = a.itw[sb + blk * ((1 << rlog) >> (sub + 1)) + v];
+    }
+    __syncthreads();
+    const u32 k = a.k, t = a.t, two_t = 2 * t, half_t = (t - 1) / 2;
+    const u32 rows = nbat * D;
+    for (u32 row = blockIdx.x; row < rows; row += gridDim.x) {
+        const u32 bb = row / D, d = row - bb * D, b = b0 + bb;
+        const u32 nb = min(a.B, nq - b * a.B);
+        const u32 lim = k * nb;                 // query slots: slot i <- h[d][b*B + i/k], i < k*n_b
+        const int8_t *src = H + (size_t)d * nq + (size_t)b * a.B;
+        auto load = [&](int i) -> u32 {
+            if ((u32)i >= lim) return 0u;
+            const int v = src[__umulhi((u32)i, kmagic)];
+            return v < 0 ? (u32)((int)t + v) : (u32)v;
+        };
+        inv_passes_perm<LG, 0, true>(buf, load, tw, t, two_t);
+        u32 *out = M + (size_t)row * N;
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+            const int pos = tid + e * NT;
+            const u32 y = csub(mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t), t);
+            out[pos] = y <= half_t ? y : (u32)((int)y - (int)t);   // centered lift (reading #3)
+        }
+        __syncthreads();   // buf is rewritten by the next row's first pass
     }
 }
 
@@ -493,8 +596,35 @@ static cudaError_t pack_dispatch(const ephdc_ctx *c, const int8_t *src, u32 nq, 
     return cudaErrorInvalidValue;
 }
 
+template <int LG>
+static cudaError_t packq_launch(const ephdc_ctx *c, const int8_t *H, u32 nq, u32 b0, u32 nbat, u32 *M, cudaStream_t st) {
+    const size_t smem = sizeof(TwPair<u32>) * (1 << LG) + sizeof(u32) * padded_len(1 << LG);
+    auto kern = k_pack_intt_q<LG>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const u32 D = c->p.D_live;
+    const int per_sm = LG >= 14 ? 1 : (16384 >> LG);
+    const uint64_t rows = (uint64_t)nbat * D;
+    const u32 grid = (u32)std::min<uint64_t>(rows, 148ull * per_sm);
+    const u32 kmagic = (u32)((1ull << 32) / c->p.k + 1);
+    kern<<<grid, (1 << LG) / kE, smem, st>>>(H, nq, b0, nbat, D, pack_args(c), kmagic, M);
+    return counted(cudaGetLastError());
+}
+
 cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t nbat,
                                      uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st) {
+    // whole-dimension calls (the hot path) use the persistent kernel; partial ranges
+    // (the parity export of single dims) the one-CTA-per-row kernel
+    if (d0 == 0 && nd == c->p.D_live && nbat > 0 && nd > 0) {
+        switch (c->p.log2N) {
+            case 10: return packq_launch<10>(c, d_H, nq, b, nbat, d_M, st);
+            case 11: return packq_launch<11>(c, d_H, nq, b, nbat, d_M, st);
+            case 12: return packq_launch<12>(c, d_H, nq, b, nbat, d_M, st);
+            case 13: return packq_launch<13>(c, d_H, nq, b, nbat, d_M, st);
+            case 14: return packq_launch<14>(c, d_H, nq, b, nbat, d_M, st);
+        }
+        return cudaErrorInvalidValue;
+    }
     return pack_dispatch<false>(c, d_H, nq, b, nbat, d0, nd, d_M, st);
 }
 
