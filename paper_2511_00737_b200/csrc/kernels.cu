@@ -409,9 +409,13 @@ struct NttArgs {
     const u64 *ninv;         // [L][2]
 };
 
+// elements per thread: 16, or 32 at 2^14 points (512 threads x 128 registers: no spills)
+template <int LG> constexpr int batch_E() { return LG >= 14 ? 32 : kE; }
+
 template <int LG, bool INV>
-__global__ void __launch_bounds__((1 << LG) / kE) k_ntt_batch(u64 *__restrict__ polys, NttArgs a) {
-    constexpr int NC = 1 << LG, NT = NC / kE;
+__global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(u64 *__restrict__ polys, NttArgs a) {
+    constexpr int E = batch_E<LG>();
+    constexpr int NC = 1 << LG, NT = NC / E;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
     const u32 S = 1u << (a.log2N - LG), N = 1u << a.log2N;
@@ -422,24 +426,24 @@ __global__ void __launch_bounds__((1 << LG) / kE) k_ntt_batch(u64 *__restrict__ 
     const TwPair<u64> *tw = a.tw + (size_t)j * N;
     auto load = [&](int pos) -> u64 { return p[pos]; };
     if constexpr (!INV) {
-        fwd_ntt<u64, LG, kE>(buf, load, tw, N + s * NC, q);
+        fwd_ntt<u64, LG, E>(buf, load, tw, N + s * NC, q);
 #pragma unroll
-        for (int e = 0; e < kE; ++e) {
+        for (int e = 0; e < E; ++e) {
             const int pos = threadIdx.x + e * NT;
             p[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
         }
     } else {
-        inv_ntt<u64, LG, kE>(buf, load, tw, q, N + s * NC);
+        inv_ntt<u64, LG, E>(buf, load, tw, q, N + s * NC);
         if (S == 1) {
             const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
 #pragma unroll
-            for (int e = 0; e < kE; ++e) {
+            for (int e = 0; e < E; ++e) {
                 const int pos = threadIdx.x + e * NT;
                 p[pos] = csub(mul_shoup_lazy<u64>(buf[pad(pos)], ni, nip, q), q);
             }
         } else {  // lazy [0, 2q): the global stages and N^-1 follow in k_ntt_global
 #pragma unroll
-            for (int e = 0; e < kE; ++e) {
+            for (int e = 0; e < E; ++e) {
                 const int pos = threadIdx.x + e * NT;
                 p[pos] = buf[pad(pos)];
             }
@@ -754,7 +758,7 @@ static cudaError_t nttb_launch(const ephdc_ntt_plan *p, u64 *polys, u32 batch, c
     a.ninv = p->ninv;
     const uint64_t grid = (uint64_t)batch * p->L << (p->log2N - LG);
     if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-    kern<<<(unsigned)grid, (1 << LG) / kE, smem, st>>>(polys, a);
+    kern<<<(unsigned)grid, (1 << LG) / batch_E<LG>(), smem, st>>>(polys, a);
     return counted(cudaGetLastError());
 }
 

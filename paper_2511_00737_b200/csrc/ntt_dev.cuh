@@ -24,6 +24,21 @@ namespace ephdc_ntt {
 EPHDC_D int pad(int i) { return i + (i >> 4); }
 constexpr int padded_len(int n) { return n + n / 16; }
 
+// Sub-stages of a forward pass with compile-time trip counts (x[] stays in registers).
+template <typename W, int T0_LOG, int R_LOG, int SUB>
+EPHDC_D void ct_substages(W (&x)[1 << R_LOG], const TwPair<W> *__restrict__ tw, u32 idx0, W q, W two_q) {
+    if constexpr (SUB < R_LOG) {
+        constexpr int R = 1 << R_LOG, h = R >> (SUB + 1);
+#pragma unroll
+        for (int v = 0; v < (1 << SUB); ++v) {
+            const TwPair<W> w = tw[(idx0 << SUB) + v];
+#pragma unroll
+            for (int kk = 0; kk < h; ++kk) ct_bfly<W>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w, q, two_q);
+        }
+        ct_substages<W, T0_LOG, R_LOG, SUB + 1>(x, tw, idx0, q, two_q);
+    }
+}
+
 // One forward pass: local stages with half-sizes 2^T0_LOG ... 2^(T0_LOG-R_LOG+1).
 template <typename W, int LG, int E, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
 EPHDC_D void fwd_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ tw, u32 tw_num, W q, W two_q) {
@@ -44,18 +59,7 @@ EPHDC_D void fwd_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ tw
             else x[k] = buf[pad(base + k * TL)];
         }
         const u32 idx0 = (tw_num >> (T0_LOG + 1)) + (u32)blk;
-#pragma unroll
-        for (int sub = 0; sub < R_LOG; ++sub) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int h = R >> (sub + 1);
-#pragma unroll
-            for (int v = 0; v < (1 << sub); ++v) {
-                const TwPair<W> w = tw[(idx0 << sub) + v];
-#pragma unroll
-                for (int kk = 0; kk < h; ++kk) ct_bfly<W>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w, q, two_q);
-            }
-        }
+        ct_substages<W, T0_LOG, R_LOG, 0>(x, tw, idx0, q, two_q);
 #pragma unroll
         for (int k = 0; k < R; ++k) buf[pad(base + k * TL)] = x[k];
     }
@@ -78,6 +82,22 @@ EPHDC_D void fwd_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ tw,
     fwd_passes<W, LG, E, LG, true>(buf, load, tw, tw_num, q, (W)(2 * q));
 }
 
+// Sub-stages of an inverse pass with compile-time trip counts.
+template <typename W, int LG, int T0_LOG, int R_LOG, int SUB>
+EPHDC_D void gs_substages(W (&x)[1 << R_LOG], const TwPair<W> *__restrict__ itw, u32 tw_num, int blk, W q, W two_q) {
+    if constexpr (SUB < R_LOG) {
+        constexpr int R = 1 << R_LOG, hs = 1 << SUB;
+#pragma unroll
+        for (int v = 0; v < R / (2 * hs); ++v) {
+            const u32 idx = (tw_num >> (T0_LOG + SUB + 1)) + (u32)((blk * R) >> (SUB + 1)) + v;
+            const TwPair<W> w = itw[idx];
+#pragma unroll
+            for (int kk = 0; kk < hs; ++kk) gs_bfly<W>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
+        }
+        gs_substages<W, LG, T0_LOG, R_LOG, SUB + 1>(x, itw, tw_num, blk, q, two_q);
+    }
+}
+
 // One inverse pass: stages with half-sizes 2^T0_LOG ... 2^(T0_LOG+R_LOG-1).
 template <typename W, int LG, int E, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
 EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, u32 tw_num, W q, W two_q) {
@@ -96,17 +116,7 @@ EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ it
             if constexpr (FROM_LOAD) x[k] = load(base + k * T0);
             else x[k] = buf[pad(base + k * T0)];
         }
-#pragma unroll
-        for (int sub = 0; sub < R_LOG; ++sub) {
-            const int hs = 1 << sub;
-#pragma unroll
-            for (int v = 0; v < R / (2 * hs); ++v) {
-                const u32 idx = (tw_num >> (T0_LOG + sub + 1)) + (u32)((blk * R) >> (sub + 1)) + v;
-                const TwPair<W> w = itw[idx];
-#pragma unroll
-                for (int kk = 0; kk < hs; ++kk) gs_bfly<W>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
-            }
-        }
+        gs_substages<W, LG, T0_LOG, R_LOG, 0>(x, itw, tw_num, blk, q, two_q);
 #pragma unroll
         for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
     }
