@@ -165,6 +165,22 @@ void ephdc_model_free(ephdc_model *m);
  * Synchronous.  EPARAM if d0+nd > D_live. */
 ephdc_status ephdc_model_export(const ephdc_model *m, uint32_t d0, uint32_t nd, uint64_t *host_out);
 
+/* Accumulator scaling ("a scaling operation ... after every g HE
+ * additions", g = 512): the client evaluation becomes
+ *   acc <- (acc + sum_{d in group J} CT_d (x) PT_d) (x) s_J^-1   for J = 0, 1, ...
+ * (groups of g consecutive dims, n_scales = ceil(D_live / g) scales, each s_J
+ * invertible mod t; the plaintext constant s_J^-1 mod t acts on NTT-form residues as
+ * its centered lift, reading #3).  Because ct (x) const distributes over the sum, this
+ * call folds the schedule into the encrypted model once: the residues of dim d are
+ * multiplied by prod_{J' >= J(d)} lift(s_J'^-1) mod q_j, after which ephdc_infer_batch
+ * returns exactly the ciphertexts of the sequential scaled evaluation (no hot-path
+ * cost).  The decrypted slot of (query, class) is then
+ *   sum_J (sum_{d in J} h[d] C[d]) prod_{J' >= J} s_J'^-1  (mod t).
+ * Mutates the model in place (do not run concurrently with infer on it).  Synchronous.
+ * Errors: ENULL, ECONTEXT, EPARAM (g = 0, wrong n_scales, s = 0 mod t), ECUDA. */
+ephdc_status ephdc_model_scale(const ephdc_ctx *ctx, ephdc_model *model, uint32_t g, const uint64_t *h_scales,
+                               uint32_t n_scales);
+
 /* ---------------- client side (the hot path; CS2) ---------------------------- */
 
 /* Device scratch for up to max_nq queries: query/hypervector staging, the

@@ -131,6 +131,48 @@ class OracleBFV:
                                   core.ptr(acc), core.ptr(cnt))
         return acc
 
+    def infer_batch_scaled(self, H: np.ndarray, nq: int, b: int, g: int, scales, model: Optional[np.ndarray] = None,
+                           class_hv: Optional[np.ndarray] = None, enc_seed: int = 0,
+                           counters: Optional[dict] = None) -> np.ndarray:
+        """Client evaluation with the accumulator scaling of PAPER.md l.429-431 ("a scaling
+        operation ... after every g HE additions", g = 512): the dims are accumulated in
+        ascending groups of g and after group j the running accumulator is multiplied by
+        the plaintext constant s_j^-1 mod t (mul_cp(acc, s_j^-1) after each
+        group, ceil(D/g) scaling multiplies).  A plaintext constant c is the constant
+        polynomial c (slot encoding of an all-c vector); in the NTT domain of q_j
+        the product is the pointwise product with lift_j(c) (centered lift, reading #3)
+        -- written here as that literal sequence, Python integers for the products."""
+        D = self.D_live
+        groups = [(d0, min(D, d0 + g)) for d0 in range(0, D, g)]
+        if len(scales) != len(groups):
+            raise ValueError("one scale per group of g dims")
+        acc = [[[0] * self.N for _ in range(self.L)] for _ in range(2)]
+        Hc = np.ascontiguousarray(H, dtype=np.int8)
+        m = None if model is None else np.ascontiguousarray(model, dtype=np.uint64)
+        C = None if class_hv is None else np.ascontiguousarray(class_hv, dtype=np.int8)
+        n_mul = n_add = n_scale = 0
+        for (d0, d1), s in zip(groups, scales):
+            if s % self.t == 0:
+                raise ValueError("scale must be invertible mod t")
+            part = np.empty((2, self.L, self.N), dtype=np.uint64)
+            cnt = np.zeros(3, dtype=np.uint64)
+            st = self._struct(enc_seed)
+            core.lib().or_infer_batch_range(ctypes.byref(st), core.ptr(Hc), nq, b, d0, d1, core.ptr(m), core.ptr(C),
+                                            core.ptr(part), core.ptr(cnt))
+            n_mul += int(cnt[0])
+            n_add += int(cnt[1]) + (1 if d0 > 0 else 0)      # folding the group into the accumulator
+            sinv = pow(int(s), -1, self.t)
+            lifted = sinv if sinv <= (self.t - 1) // 2 else sinv - self.t
+            for c in range(2):
+                for j, p in enumerate(self.q):
+                    f = lifted % p
+                    pj = part[c, j].tolist()
+                    acc[c][j] = [((a + x) * f) % p for a, x in zip(acc[c][j], pj)]
+            n_scale += 1
+        if counters is not None:
+            counters.update(mul_cp=n_mul, add_cc=n_add, scale=n_scale, rot=0)
+        return np.array(acc, dtype=np.uint64)
+
     # -- server: decrypt / decode (CS3) ------------------------------------------
     def decrypt_poly(self, ct: np.ndarray) -> List[int]:
         """Phase x = c0 + c1*s in coefficient form, CRT-combined into [0, Q) (Python ints)."""

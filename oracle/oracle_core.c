@@ -332,8 +332,18 @@ void or_plaintext_ntts(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0, 
    model == NULL: each dim's ciphertext is re-encrypted on the fly from class_hv
    (c4's model does not fit in host RAM); otherwise model is [D_live][L][2][N].
    counters (may be NULL): [0] MulCP, [1] AddCC, [2] rotations. */
+void or_infer_batch_range(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0, u32 d1,
+                          const u64 *model, const int8_t *class_hv, u64 *acc, u64 *counters);
+
 void or_infer_batch(const or_bfv *P, const int8_t *H, u32 nq, u32 b,
                     const u64 *model, const int8_t *class_hv, u64 *acc, u64 *counters) {
+    or_infer_batch_range(P, H, nq, b, 0, P->D_live, model, class_hv, acc, counters);
+}
+
+/* The same sum over the dims [d0, d1) only (model, when given, is still indexed by the
+   absolute dim); used by the scaled evaluation of oracle/bfv.py (groups of g dims). */
+void or_infer_batch_range(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0, u32 d1,
+                          const u64 *model, const int8_t *class_hv, u64 *acc, u64 *counters) {
     u32 N = 1u << P->logN;
     u32 L = P->L;
     u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
@@ -352,7 +362,7 @@ void or_infer_batch(const or_bfv *P, const int8_t *H, u32 nq, u32 b,
         u64 *part = (u64 *)calloc((size_t)2 * L * N, sizeof(u64));
         int have = 0;
         #pragma omp for schedule(dynamic, 4)
-        for (long long dd = 0; dd < (long long)P->D_live; ++dd) {
+        for (long long dd = d0; dd < (long long)d1; ++dd) {
             u32 d = (u32)dd;
             const u64 *c;
             if (model) c = model + (u64)d * L * 2 * N;

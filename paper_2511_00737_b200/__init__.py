@@ -160,6 +160,13 @@ class EncryptedModel:
         call("ephdc_model_export", self._h, d0, nd, _np_ptr(out))
         return out
 
+    def scale(self, g: int, scales: Sequence[int]) -> "EncryptedModel":
+        """ephdc_model_scale: fold the accumulator-scaling schedule (one scale per group of
+        g dims) into the model, in place."""
+        s = np.ascontiguousarray(np.array([int(x) for x in scales] or [1], dtype=np.uint64))
+        call("ephdc_model_scale", self.ctx.handle, self._h, g, _np_ptr(s), len(scales))
+        return self
+
     def __del__(self):
         try:
             if self._h:

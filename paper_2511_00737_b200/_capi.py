@@ -65,6 +65,7 @@ _SIGS = {
     "ephdc_encrypt_model": (c_st, [c_vp, c_vp, c_vp, c_u64, c_vp]),
     "ephdc_model_free": (None, [c_vp]),
     "ephdc_model_export": (c_st, [c_vp, c_u32, c_u32, c_vp]),
+    "ephdc_model_scale": (c_st, [c_vp, c_vp, c_u32, c_vp, c_u32]),
     "ephdc_workspace_create": (c_st, [c_vp, c_u32, c_vp]),
     "ephdc_workspace_free": (None, [c_vp]),
     "ephdc_workspace_set_timing": (c_st, [c_vp, c_int]),

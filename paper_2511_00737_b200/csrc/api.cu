@@ -383,6 +383,37 @@ ephdc_status ephdc_model_export(const ephdc_model *m, uint32_t d0, uint32_t nd, 
     return EPHDC_OK;
 }
 
+ephdc_status ephdc_model_scale(const ephdc_ctx *c, ephdc_model *m, uint32_t g, const uint64_t *h_scales,
+                               uint32_t n_scales) {
+    if (!c || !m || (!h_scales && n_scales)) return EPHDC_ENULL;
+    if (m->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    const uint32_t D = m->D, L = c->L;
+    if (g == 0 || n_scales != (D + g - 1) / g) return EPHDC_EPARAM;
+    for (uint32_t J = 0; J < n_scales; ++J)
+        if (h_scales[J] % c->t == 0) return EPHDC_EPARAM;
+    // cumulative factor of group J per prime: prod_{J' >= J} lift(s_J'^-1 mod t) mod q_j
+    std::vector<uint64_t> fac((size_t)n_scales * L);
+    std::vector<uint64_t> run(L, 1);
+    for (uint32_t J = n_scales; J-- > 0;) {
+        const uint64_t inv = invmod(h_scales[J] % c->t, c->t);
+        const bool neg = inv > (c->t - 1) / 2;
+        for (uint32_t j = 0; j < L; ++j) {
+            const uint64_t q = c->q[j];
+            const uint64_t lift = neg ? q - (c->t - inv) : inv;   // centered lift into [0, q)
+            run[j] = mulmod(run[j], lift, q);
+            // integer path: Montgomery form (x 2^64) for mont_mul; FP64 path: plain factor
+            fac[(size_t)J * L + j] = c->f64.enabled ? run[j] : (uint64_t)(((u128)run[j] << 64) % q);
+        }
+    }
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    DevBuf bf;
+    if (cudaMalloc(&bf.p, sizeof(uint64_t) * fac.size()) != cudaSuccess) return EPHDC_ERESOURCE;
+    EPHDC_CUDA_TRY(cudaMemcpy(bf.p, fac.data(), sizeof(uint64_t) * fac.size(), cudaMemcpyHostToDevice));
+    EPHDC_CUDA_TRY(launch_model_scale(c, m->d_ct, D, g, (const uint64_t *)bf.p, 0));
+    EPHDC_CUDA_TRY(cudaDeviceSynchronize());
+    return EPHDC_OK;
+}
+
 // ------------------------------------------------------------------------------------
 // workspace
 // ------------------------------------------------------------------------------------

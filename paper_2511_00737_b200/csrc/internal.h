@@ -145,6 +145,9 @@ cudaError_t launch_encode_tc(const ephdc_ctx *c, const void *d_X, const int8_t *
 cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
                                uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st);
+// model residues of dim d times fac[d / g][j] (ephdc_model_scale)
+cudaError_t launch_model_scale(const ephdc_ctx *c, uint64_t *d_model, uint32_t D, uint32_t g, const uint64_t *d_fac,
+                               cudaStream_t st);
 cudaError_t launch_plaintext_ntt_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
                                      cudaStream_t st);
 cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, cudaStream_t st);

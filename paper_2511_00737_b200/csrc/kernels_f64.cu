@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "modarith.cuh"
 #include "ntt_f64.cuh"
 #include "tmem.cuh"
 #include "async_copy.cuh"
@@ -308,6 +309,37 @@ __global__ void k_u64_to_f64(u64 *__restrict__ d, size_t n) {
 cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_u64_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d, n);
+    return counted(cudaGetLastError());
+}
+
+// model residue of (dim d, prime j) times fac[d / g][j] mod q_j (ephdc_model_scale):
+// FP64 path (exact doubles, fac plain) or integer path (u64, fac in Montgomery form)
+template <bool F64>
+__global__ void k_model_scale(u64 *__restrict__ m, size_t n, u32 L, u32 N, u32 g, const u64 *__restrict__ fac,
+                              PrimeSet ps) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const size_t dj = i / ((size_t)2 * N);           // (d, j) of [D][L][2][N]
+    const u32 j = (u32)(dj % L), d = (u32)(dj / L);
+    const u64 q = ps.q[j], f = fac[(size_t)(d / g) * L + j];
+    if constexpr (F64) {
+        const double qd = (double)q;
+        double r = mul_rt(__longlong_as_double((long long)m[i]), (double)f, 1.0 / qd, -qd);
+        r = reduce(r, 1.0 / qd, -qd);
+        if (r < 0) r = __dadd_rn(r, qd);
+        m[i] = (u64)__double_as_longlong(r);
+    } else {
+        m[i] = mont_mul(m[i], f, q, ps.qinv[j]);
+    }
+}
+
+cudaError_t launch_model_scale(const ephdc_ctx *c, uint64_t *d_model, uint32_t D, uint32_t g, const uint64_t *d_fac,
+                               cudaStream_t st) {
+    const size_t n = (size_t)D * c->L * 2 * c->N;
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (c->f64.enabled) k_model_scale<true><<<blocks, 256, 0, st>>>(d_model, n, c->L, c->N, g, d_fac, c->ps);
+    else k_model_scale<false><<<blocks, 256, 0, st>>>(d_model, n, c->L, c->N, g, d_fac, c->ps);
     return counted(cudaGetLastError());
 }
 
