@@ -280,10 +280,12 @@ def main():
     # e2e: the same step through the host-buffer C-ABI call (H2D + compute + D2H per step)
     e2e = None
     if not a.no_e2e:
+        # the call a client makes: features from host memory in, the scores message it
+        # sends to the server (bit-packed ciphertexts, ephdc_classify_host_packed) out
         Xh = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).pin_memory()
-        oh = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, pin_memory=True)
+        oh = torch.empty(eph.scores_message_bytes(ctx, nb), dtype=torch.uint8, pin_memory=True)
         for _ in range(max(1, a.warmup)):
-            eph.classify_host(ctx, model, ws, Xh, ps.P_dev, oh)
+            eph.classify_host_packed(ctx, model, ws, Xh, ps.P_dev, oh)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -291,12 +293,13 @@ def main():
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(a.steps):
-            eph.classify_host(ctx, model, ws, Xh, ps.P_dev, oh)
+            eph.classify_host_packed(ctx, model, ws, Xh, ps.P_dev, oh)
         f1.record(stream)
         torch.cuda.synchronize(dev)
         ems = pdist.max_over_ranks(f0.elapsed_time(f1) / a.steps)
         e2e = {"value": world * nq / (ems / 1e3), "unit": "queries/s",
-               "h2d_bytes_per_step": int(Xh.numel()), "d2h_bytes_per_step": int(oh.numel() * 8)}
+               "h2d_bytes_per_step": int(Xh.numel()), "d2h_bytes_per_step": int(oh.numel()),
+               "call": "ephdc_classify_host_packed (features in, bit-packed scores message out)"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:

@@ -233,6 +233,27 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *ctx, const ephdc_model *model,
                                  const void *h_X, const int8_t *d_P, uint32_t nq, uint64_t *h_out,
                                  uint32_t cap_ct, void *stream);
 
+/* ---------------- scores message (client -> server) -------- */
+
+/* The message the client sends per call: the nb scores ciphertexts ("only the
+ * encrypted similarity scores") with the residues of prime j bit-packed at b_j =
+ * bit_length(q_j) bits (little-endian bit order within a block), blocks in [nb][2][L]
+ * order, each block N*b_j/8 bytes; no header (the parameters are the context's).
+ * Size: nb * 2 * N * sum_j b_j / 8 bytes (c4: 1.77 MB per ciphertext vs 2.36 MB of
+ * u64 words).  SURVEY NEXT #4. */
+size_t ephdc_scores_message_bytes(const ephdc_ctx *ctx, uint32_t nb);
+/* Device -> device packing of d_ct [nb][2][L][N] (canonical) into d_msg.  Async. */
+ephdc_status ephdc_pack_scores(const ephdc_ctx *ctx, const uint64_t *d_ct, uint32_t nb, uint8_t *d_msg, void *stream);
+/* Host unpacking (server side): h_msg -> h_ct [nb][2][L][N].  EDOMAIN if a residue
+ * is >= its prime.  Synchronous. */
+ephdc_status ephdc_unpack_scores(const ephdc_ctx *ctx, const uint8_t *h_msg, uint32_t nb, uint64_t *h_ct);
+/* End-to-end client call producing the message: h_X -> device, encode_queries +
+ * infer_batch + pack_scores, message -> h_msg (ephdc_scores_message_bytes(ctx, nb)
+ * bytes).  Synchronous on `stream`. */
+ephdc_status ephdc_classify_host_packed(const ephdc_ctx *ctx, const ephdc_model *model, ephdc_workspace *ws,
+                                        const void *h_X, const int8_t *d_P, uint32_t nq, uint8_t *h_msg,
+                                        void *stream);
+
 /* ---------------- server decide (test-only host; CS3) ----------------------- */
 
 /* Decrypts nb = ceil(nq/B) scores ciphertexts h_ct [nb][2][L][N]:

@@ -20,6 +20,7 @@ __all__ = [
     "Context", "SecretKey", "EncryptedModel", "Workspace", "NttPlan", "EphdcError",
     "find_ntt_primes", "min_psi", "gaussian_cdt", "launch_count",
     "encode_queries", "encode_raw", "infer_batch", "encode_plaintexts", "classify_host",
+    "scores_message_bytes", "pack_scores", "unpack_scores", "classify_host_packed",
     "decrypt_scores", "decrypt_slots", "ntt_fwd", "ntt_inv", "mac",
 ]
 
@@ -256,6 +257,39 @@ def classify_host(ctx: Context, model: EncryptedModel, ws: Workspace, X_host, P,
     call("ephdc_classify_host", ctx.handle, model.handle, ws.handle, X_host.data_ptr(), _dptr(P), nq,
          out_host.data_ptr(), out_host.shape[0], _stream(stream))
     return out_host
+
+
+# --------------------------------------------------------------------------- scores message
+def scores_message_bytes(ctx: Context, nb: int) -> int:
+    return int(lib.ephdc_scores_message_bytes(ctx.handle, nb))
+
+
+def pack_scores(ctx: Context, cts, msg=None, stream=None):
+    """cts: cuda [nb, 2, L, N] -> cuda uint8 message (bit-packed residues)."""
+    import torch
+    nb = cts.shape[0]
+    if msg is None:
+        msg = torch.empty(scores_message_bytes(ctx, nb), dtype=torch.uint8, device=cts.device)
+    call("ephdc_pack_scores", ctx.handle, _dptr(cts), nb, _dptr(msg), _stream(stream))
+    return msg
+
+
+def unpack_scores(ctx: Context, msg: np.ndarray, nb: int) -> np.ndarray:
+    m = np.ascontiguousarray(msg, dtype=np.uint8)
+    out = np.zeros((nb, 2, ctx.L, ctx.N), dtype=np.uint64)
+    call("ephdc_unpack_scores", ctx.handle, _np_ptr(m), nb, _np_ptr(out))
+    return out
+
+
+def classify_host_packed(ctx: Context, model: EncryptedModel, ws: Workspace, X_host, P, msg_host=None, stream=None):
+    """End-to-end client call returning the message sent to the server (pinned CPU uint8)."""
+    import torch
+    nq = X_host.shape[0]
+    if msg_host is None:
+        msg_host = torch.empty(scores_message_bytes(ctx, ctx.n_batches(nq)), dtype=torch.uint8, pin_memory=True)
+    call("ephdc_classify_host_packed", ctx.handle, model.handle, ws.handle, X_host.data_ptr(), _dptr(P), nq,
+         msg_host.data_ptr(), _stream(stream))
+    return msg_host
 
 
 # --------------------------------------------------------------------------- server decide (host)

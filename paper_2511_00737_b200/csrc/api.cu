@@ -196,6 +196,11 @@ ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out
     for (uint32_t j = 0; j < c->L; ++j) c->host_q[j].init(c->q[j], c->psi[j], p->log2N);
     c->host_t.init(p->t, c->psi_t, p->log2N);
     c->crt.init(c->q, p->t);
+    for (uint64_t qj : c->q) {
+        uint32_t b = 0;
+        while (b < 64 && (qj >> b)) ++b;
+        c->qbits.push_back(b);
+    }
     // fused MAC kernel geometry: S CTAs per polynomial (N = 16384 -> 2 halves of 8192),
     // dims split in chunks so the grid holds ~8 waves; all partial sums < 2^64.
     c->fused_S = p->log2N >= 14 ? (1u << (p->log2N - 13)) : 1u;
@@ -424,6 +429,7 @@ void ephdc_workspace_free(ephdc_workspace *ws) {
     cudaFree(ws->d_X);
     cudaFree(ws->d_H);
     cudaFree(ws->d_out);
+    cudaFree(ws->d_msg);
     for (cudaEvent_t e : ws->ev_pool) cudaEventDestroy(e);
     delete ws;
 }
@@ -450,7 +456,8 @@ ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_w
     }
     if (dev_alloc(&ws->d_M, D * c->N * ws->m_batches) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
         dev_alloc(&ws->d_H, D * max_nq) != cudaSuccess ||
-        dev_alloc(&ws->d_out, (size_t)ws->nb_max * 2 * c->L * c->N) != cudaSuccess) {
+        dev_alloc(&ws->d_out, (size_t)ws->nb_max * 2 * c->L * c->N) != cudaSuccess ||
+        dev_alloc(&ws->d_msg, ephdc_scores_message_bytes(c, ws->nb_max)) != cudaSuccess) {
         ephdc_workspace_free(ws.release());
         return EPHDC_ERESOURCE;
     }
@@ -607,6 +614,64 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *c, const ephdc_model *m, ephdc
     s = infer_impl(c, m, ws, ws->d_H, nq, ws->d_out, st);
     if (s != EPHDC_OK) return s;
     EPHDC_CUDA_TRY(cudaMemcpyAsync(h_out, ws->d_out, sizeof(uint64_t) * 2 * c->L * c->N * nb, cudaMemcpyDeviceToHost, st));
+    EPHDC_CUDA_TRY(cudaStreamSynchronize(st));
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// scores message (bit-packed residues)
+// ------------------------------------------------------------------------------------
+size_t ephdc_scores_message_bytes(const ephdc_ctx *c, uint32_t nb) {
+    if (!c) return 0;
+    size_t bits = 0;
+    for (uint32_t b : c->qbits) bits += b;
+    return (size_t)nb * 2 * c->N * bits / 8;
+}
+
+ephdc_status ephdc_pack_scores(const ephdc_ctx *c, const uint64_t *d_ct, uint32_t nb, uint8_t *d_msg, void *stream) {
+    if (!c || ((!d_ct || !d_msg) && nb)) return EPHDC_ENULL;
+    if (c->device < 0) return EPHDC_ECONTEXT;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    EPHDC_CUDA_TRY(launch_pack_bits(c, d_ct, nb, d_msg, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_unpack_scores(const ephdc_ctx *c, const uint8_t *h_msg, uint32_t nb, uint64_t *h_ct) {
+    if (!c || ((!h_msg || !h_ct) && nb)) return EPHDC_ENULL;
+    const uint32_t N = c->N, L = c->L;
+    size_t bitpos = 0;
+    for (uint32_t bc = 0; bc < 2 * nb; ++bc)
+        for (uint32_t j = 0; j < L; ++j) {
+            const uint32_t bj = c->qbits[j];
+            uint64_t *o = h_ct + ((size_t)bc * L + j) * N;
+            for (uint32_t i = 0; i < N; ++i) {
+                uint64_t v = 0;
+                for (uint32_t k = 0; k < bj; ++k, ++bitpos)
+                    v |= (uint64_t)((h_msg[bitpos >> 3] >> (bitpos & 7)) & 1u) << k;
+                if (v >= c->q[j]) return EPHDC_EDOMAIN;
+                o[i] = v;
+            }
+        }
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_classify_host_packed(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws,
+                                        const void *h_X, const int8_t *d_P, uint32_t nq, uint8_t *h_msg,
+                                        void *stream) {
+    if (!c || !m || !ws || ((!h_X || !d_P || !h_msg) && nq)) return EPHDC_ENULL;
+    if (m->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    if (nq > ws->max_nq) return EPHDC_EPARAM;
+    if (nq == 0) return EPHDC_OK;
+    const uint32_t nb = (nq + c->B - 1) / c->B;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    EPHDC_CUDA_TRY(cudaMemcpyAsync(ws->d_X, h_X, (size_t)nq * c->p.F, cudaMemcpyHostToDevice, st));
+    ephdc_status s = encode_impl(c, ws, ws->d_X, d_P, nq, ws->d_H, st);
+    if (s != EPHDC_OK) return s;
+    s = infer_impl(c, m, ws, ws->d_H, nq, ws->d_out, st);
+    if (s != EPHDC_OK) return s;
+    EPHDC_CUDA_TRY(launch_pack_bits(c, ws->d_out, nb, ws->d_msg, st));
+    EPHDC_CUDA_TRY(cudaMemcpyAsync(h_msg, ws->d_msg, ephdc_scores_message_bytes(c, nb), cudaMemcpyDeviceToHost, st));
     EPHDC_CUDA_TRY(cudaStreamSynchronize(st));
     return EPHDC_OK;
 }

@@ -71,6 +71,7 @@ struct ephdc_ctx {
     ephdc::ctxDev dev;
     uint32_t fused_S = 1, fused_chunks = 1, fused_G = 1;
     ephdc::F64Plan f64;
+    std::vector<uint32_t> qbits;   // bit_length(q_j): scores-message packing widths
 };
 
 struct ephdc_sk {
@@ -93,6 +94,7 @@ struct ephdc_workspace {
     void *d_X = nullptr;          // [max_nq][F]
     int8_t *d_H = nullptr;        // [D_live][max_nq]
     uint64_t *d_out = nullptr;    // [nb_max][2][L][N]
+    uint8_t *d_msg = nullptr;     // packed scores message of nb_max ciphertexts
     uint32_t nb_max = 0;
     // timing
     bool timing = false;
@@ -145,6 +147,14 @@ cudaError_t launch_encode_tc(const ephdc_ctx *c, const void *d_X, const int8_t *
 cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
                                uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st);
+// scores message layout (bit-packed residues, ephdc.h "scores message")
+struct MsgLayout {
+    u32 bits[kMaxL];     // bit_length(q_j)
+    u64 prefix[kMaxL];   // byte offset of prime j inside a (batch, component) group
+    u64 group_bytes;     // bytes of one (batch, component) group = N * sum_j bits / 8
+};
+MsgLayout msg_layout(const ephdc_ctx *c);
+cudaError_t launch_pack_bits(const ephdc_ctx *c, const uint64_t *d_ct, uint32_t nb, uint8_t *d_msg, cudaStream_t st);
 // model residues of dim d times fac[d / g][j] (ephdc_model_scale)
 cudaError_t launch_model_scale(const ephdc_ctx *c, uint64_t *d_model, uint32_t D, uint32_t g, const uint64_t *d_fac,
                                cudaStream_t st);

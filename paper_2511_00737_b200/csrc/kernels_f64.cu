@@ -343,6 +343,50 @@ cudaError_t launch_model_scale(const ephdc_ctx *c, uint64_t *d_model, uint32_t D
     return counted(cudaGetLastError());
 }
 
+// Scores message: block (b, c, j) of N residues bit-packed at bits[j] bits; thread =
+// 8 consecutive residues = bits[j] bytes.
+__global__ void k_pack_bits(const u64 *__restrict__ ct, u32 nblocks, u32 L, u32 N, MsgLayout m,
+                            uint8_t *__restrict__ msg) {
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 per = N / 8;
+    if (gid >= (size_t)nblocks * per) return;
+    const u32 blk = (u32)(gid / per), g = (u32)(gid % per), j = blk % L, bc = blk / L, bj = m.bits[j];
+    const u64 *x = ct + (size_t)blk * N + 8 * g;
+    uint8_t *o = msg + (size_t)bc * m.group_bytes + m.prefix[j] + (size_t)g * bj;
+    unsigned __int128 acc = 0;
+    int have = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        acc |= (unsigned __int128)x[r] << have;
+        have += (int)bj;
+        while (have >= 8) {
+            *o++ = (uint8_t)(acc & 0xFF);
+            acc >>= 8;
+            have -= 8;
+        }
+    }
+}
+
+MsgLayout msg_layout(const ephdc_ctx *c) {
+    MsgLayout m{};
+    u64 off = 0;
+    for (u32 j = 0; j < c->L; ++j) {
+        m.bits[j] = c->qbits[j];
+        m.prefix[j] = off;
+        off += (u64)c->N * c->qbits[j] / 8;
+    }
+    m.group_bytes = off;
+    return m;
+}
+
+cudaError_t launch_pack_bits(const ephdc_ctx *c, const uint64_t *d_ct, uint32_t nb, uint8_t *d_msg, cudaStream_t st) {
+    const u32 nblocks = nb * 2 * c->L;
+    const size_t threads = (size_t)nblocks * (c->N / 8);
+    if (threads == 0) return cudaSuccess;
+    k_pack_bits<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_ct, nblocks, c->L, c->N, msg_layout(c), d_msg);
+    return counted(cudaGetLastError());
+}
+
 // out[b][c][j][i] <- out mod q_j
 __global__ void k_reduce_out(u64 *__restrict__ out, u32 L, u32 N, PrimeSet ps, size_t n_total) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
