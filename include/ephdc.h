@@ -233,6 +233,28 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *ctx, const ephdc_model *model,
                                  const void *h_X, const int8_t *d_P, uint32_t nq, uint64_t *h_out,
                                  uint32_t cap_ct, void *stream);
 
+/* ---------------- HE-HDC-SR: the server-side SIMD baseline -- */
+/* P:257-265 / SPEC S:445-453: the CLIENT encrypts its query hypervectors in the same
+ * interleave layout (slot i of ciphertext d = h[d][b*B + i/k], D_live ciphertexts per
+ * batch of B queries) and uploads them; the SERVER multiplies them by the plaintext
+ * class tiles (slot i = C[i mod k][d]) and sums over d -- the same arithmetic as
+ * ephdc_infer_batch with the ct/pt roles of model and queries swapped (P:786 compares
+ * the two: the client runtime is dominated by this encryption, the message is D_live
+ * ciphertexts per batch instead of one). */
+
+/* Client: batch b of d_H [D_live][nq] -> d_qct [D_live][L][2][N]: secret-key BFV with
+ * the client's key (readings #4-#10), random streams of ciphertext index b*D_live + d.
+ * Uses the workspace's plaintext buffer.  Async. */
+ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *ctx, ephdc_sk *sk, ephdc_workspace *ws, const int8_t *d_H,
+                                      uint32_t nq, uint32_t b, uint64_t seed, uint64_t *d_qct, void *stream);
+/* Server, once: the plaintext class tiles in NTT form, d_pt [D_live][L][N] canonical:
+ * NTT_j(centered lift(encode(tile_d))).  h_class_hv: HOST int8 [k][D_live].  Synchronous. */
+ephdc_status ephdc_sr_model_plaintexts(const ephdc_ctx *ctx, const int8_t *h_class_hv, uint64_t *d_pt);
+/* Server: d_out [2][L][N] = sum_d d_qct[d] (x) d_pt[d]: D_live MulCP, D_live-1 AddCC,
+ * 0 rotations.  Decrypts with the client's key (ephdc_decrypt_scores).  Async. */
+ephdc_status ephdc_sr_evaluate(const ephdc_ctx *ctx, const uint64_t *d_pt, const uint64_t *d_qct, uint64_t *d_out,
+                               void *stream);
+
 /* ---------------- scores message (client -> server) -------- */
 
 /* The message the client sends per call: the nb scores ciphertexts ("only the

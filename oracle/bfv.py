@@ -173,6 +173,24 @@ class OracleBFV:
             counters.update(mul_cp=n_mul, add_cc=n_add, scale=n_scale, rot=0)
         return np.array(acc, dtype=np.uint64)
 
+    # -- HE-HDC-SR, the server-side SIMD baseline -----------
+    def sr_encrypt_queries(self, H: np.ndarray, nq: int, b: int, enc_seed: int) -> np.ndarray:
+        """Client: batch b's query hypervectors as D_live ciphertexts [D][L][2][N]."""
+        Hc = np.ascontiguousarray(H, dtype=np.int8)
+        out = np.empty((self.D_live, self.L, 2, self.N), dtype=np.uint64)
+        st = self._struct(enc_seed)
+        core.lib().or_encrypt_queries(ctypes.byref(st), core.ptr(Hc), nq, b, 0, self.D_live, core.ptr(out))
+        return out
+
+    def sr_server_eval(self, class_hv: np.ndarray, qct: np.ndarray) -> np.ndarray:
+        """Server: sum_d qct_d (.) encode(tile_d) with the plaintext class tiles -> [2][L][N]."""
+        C = np.ascontiguousarray(class_hv, dtype=np.int8)
+        q = np.ascontiguousarray(qct, dtype=np.uint64)
+        acc = np.empty((2, self.L, self.N), dtype=np.uint64)
+        st = self._struct()
+        core.lib().or_server_eval(ctypes.byref(st), core.ptr(C), core.ptr(q), core.ptr(acc))
+        return acc
+
     # -- server: decrypt / decode (CS3) ------------------------------------------
     def decrypt_poly(self, ct: np.ndarray) -> List[int]:
         """Phase x = c0 + c1*s in coefficient form, CRT-combined into [0, Q) (Python ints)."""

@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
             "or_plaintext_ntts": (None, [ctypes.POINTER(OrBfv), P, u32, u32, u32, u32, P]),
             "or_infer_batch": (None, [ctypes.POINTER(OrBfv), P, u32, u32, P, P, P, P]),
             "or_infer_batch_range": (None, [ctypes.POINTER(OrBfv), P, u32, u32, u32, u32, P, P, P, P]),
+            "or_encrypt_queries": (None, [ctypes.POINTER(OrBfv), P, u32, u32, u32, u32, P]),
+            "or_server_eval": (None, [ctypes.POINTER(OrBfv), P, P, P]),
             "or_decrypt_phase": (None, [ctypes.POINTER(OrBfv), P, P]),
         }
         for name, (res, args) in sig.items():

@@ -234,11 +234,22 @@ static void model_plaintext(const or_bfv *P, const int8_t *class_hv, u32 d, cons
     or_ntt_inv(m, P->logN, P->t, tinv_tab);
 }
 
+/* secret-key encryption of the encoded message m ([0,t)) with the random streams of
+   ciphertext index g: out[L][2][N] canonical NTT form */
+static void encrypt_msg(const or_bfv *P, u64 g, const u64 *m, u64 *const *psi_tabs, long long *e, u64 *x,
+                        u64 *out);
+
 /* ciphertext of dim d, all primes: out[L][2][N] canonical NTT form */
 static void encrypt_dim(const or_bfv *P, const int8_t *class_hv, u32 d, const u64 *tinv_tab,
                         u64 *const *psi_tabs, u64 *m, long long *e, u64 *x, u64 *out) {
-    u32 N = 1u << P->logN;
     model_plaintext(P, class_hv, d, tinv_tab, m);
+    encrypt_msg(P, d, m, psi_tabs, e, x, out);
+}
+
+static void encrypt_msg(const or_bfv *P, u64 g, const u64 *m, u64 *const *psi_tabs, long long *e, u64 *x,
+                        u64 *out) {
+    u32 N = 1u << P->logN;
+    u64 d = g;
     or_sample_gauss_poly(P->enc_seed, d, N, P->cdt, P->ncdt, e);
     for (u32 j = 0; j < P->L; ++j) {
         u64 q = P->q[j];
@@ -416,4 +427,64 @@ void or_decrypt_phase(const or_bfv *P, const u64 *ct, u64 *out) {
         or_ntt_inv(o, P->logN, q, inv[j]);
     }
     free_tabs(inv, P->L);
+}
+
+
+/* ------------------------------------------------------------------ */
+/* HE-HDC-SR, the server-side SIMD baseline (P:257-265;    */
+/* SPEC S:445-453): the CLIENT encrypts its query hypervectors in the  */
+/* interleave layout (D ciphertexts per batch of B queries), the       */
+/* SERVER multiplies them by the plaintext class tiles.                */
+/* ------------------------------------------------------------------ */
+
+/* query ciphertexts of batch b, dims [d0, d0+nd): out[nd][L][2][N]; message = the query
+   slot vector of (b, d) encoded mod t ([0,t), Delta*m as for the model, reading #4);
+   random streams of ciphertext index g = b*D_live + d. */
+void or_encrypt_queries(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0, u32 nd, u64 *out) {
+    u32 N = 1u << P->logN;
+    u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(or_powmod(P->psi_t, P->t - 2, P->t), P->t, P->logN, tinv);
+    u64 **fw = make_psi_tabs(P, 0);
+    #pragma omp parallel
+    {
+        u64 *m = (u64 *)malloc(sizeof(u64) * N);
+        u64 *x = (u64 *)malloc(sizeof(u64) * N);
+        long long *e = (long long *)malloc(sizeof(long long) * N);
+        #pragma omp for schedule(dynamic)
+        for (long long dd = 0; dd < (long long)nd; ++dd) {
+            u32 d = d0 + (u32)dd;
+            query_plaintext(P, H, nq, b, d, tinv, m);
+            encrypt_msg(P, (u64)b * P->D_live + d, m, fw, e, x, out + (u64)dd * P->L * 2 * N);
+        }
+        free(m); free(x); free(e);
+    }
+    free(tinv);
+    free_tabs(fw, P->L);
+}
+
+/* server: acc[c][j] = sum_d qct_{d,j,c} (.) NTT_j(lift(encode(tile_d))), qct [D_live][L][2][N] */
+void or_server_eval(const or_bfv *P, const int8_t *class_hv, const u64 *qct, u64 *acc) {
+    u32 N = 1u << P->logN;
+    u32 L = P->L;
+    u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
+    or_pow_brev_table(or_powmod(P->psi_t, P->t - 2, P->t), P->t, P->logN, tinv);
+    u64 **fw = make_psi_tabs(P, 0);
+    u64 *m = (u64 *)malloc(sizeof(u64) * N);
+    u64 *p = (u64 *)malloc(sizeof(u64) * N);
+    for (u64 x = 0; x < (u64)2 * L * N; ++x) acc[x] = 0;
+    for (u32 d = 0; d < P->D_live; ++d) {
+        model_plaintext(P, class_hv, d, tinv, m);
+        for (u32 j = 0; j < L; ++j) {
+            u64 q = P->q[j];
+            for (u32 i = 0; i < N; ++i) p[i] = lift_centered(m[i], P->t, q);
+            or_ntt_fwd(p, P->logN, q, fw[j]);
+            for (u32 cc = 0; cc < 2; ++cc) {
+                const u64 *cj = qct + (((u64)d * L + j) * 2 + cc) * N;
+                u64 *aj = acc + ((u64)cc * L + j) * N;
+                for (u32 i = 0; i < N; ++i) aj[i] = or_addmod(aj[i], or_mulmod(cj[i], p[i], q), q);
+            }
+        }
+    }
+    free(m); free(p); free(tinv);
+    free_tabs(fw, L);
 }

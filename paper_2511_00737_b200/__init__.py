@@ -21,6 +21,7 @@ __all__ = [
     "find_ntt_primes", "min_psi", "gaussian_cdt", "launch_count",
     "encode_queries", "encode_raw", "infer_batch", "encode_plaintexts", "classify_host",
     "scores_message_bytes", "pack_scores", "unpack_scores", "classify_host_packed",
+    "sr_encrypt_queries", "sr_model_plaintexts", "sr_evaluate",
     "decrypt_scores", "decrypt_slots", "ntt_fwd", "ntt_inv", "mac",
 ]
 
@@ -257,6 +258,37 @@ def classify_host(ctx: Context, model: EncryptedModel, ws: Workspace, X_host, P,
     call("ephdc_classify_host", ctx.handle, model.handle, ws.handle, X_host.data_ptr(), _dptr(P), nq,
          out_host.data_ptr(), out_host.shape[0], _stream(stream))
     return out_host
+
+
+# --------------------------------------------------------------------------- HE-HDC-SR baseline
+def sr_encrypt_queries(ctx: Context, sk: SecretKey, ws: Workspace, H, nq: int, b: int, seed: int, out=None,
+                       stream=None):
+    """Client of HE-HDC-SR: batch b of H cuda [D_live, nq] -> cuda [D_live, L, 2, N] ciphertexts."""
+    import torch
+    if out is None:
+        out = torch.empty((ctx.D_live, ctx.L, 2, ctx.N), dtype=torch.int64, device=H.device)
+    call("ephdc_sr_encrypt_queries", ctx.handle, sk.handle, ws.handle, _dptr(H), nq, b, seed, _dptr(out),
+         _stream(stream))
+    return out
+
+
+def sr_model_plaintexts(ctx: Context, class_hv: np.ndarray, out=None):
+    """Server of HE-HDC-SR, once: plaintext class tiles in NTT form, cuda [D_live, L, N]."""
+    import torch
+    C = np.ascontiguousarray(class_hv, dtype=np.int8)
+    if out is None:
+        out = torch.empty((ctx.D_live, ctx.L, ctx.N), dtype=torch.int64, device=torch.device("cuda", ctx.device))
+    call("ephdc_sr_model_plaintexts", ctx.handle, _np_ptr(C), _dptr(out))
+    return out
+
+
+def sr_evaluate(ctx: Context, pt, qct, out=None, stream=None):
+    """Server of HE-HDC-SR: sum_d qct[d] * pt[d] -> cuda [2, L, N] scores ciphertext."""
+    import torch
+    if out is None:
+        out = torch.empty((2, ctx.L, ctx.N), dtype=torch.int64, device=qct.device)
+    call("ephdc_sr_evaluate", ctx.handle, _dptr(pt), _dptr(qct), _dptr(out), _stream(stream))
+    return out
 
 
 # --------------------------------------------------------------------------- scores message

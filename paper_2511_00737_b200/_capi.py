@@ -76,6 +76,9 @@ _SIGS = {
     "ephdc_encode_plaintexts": (c_st, [c_vp, c_vp, c_vp, c_u32, c_u32, c_u32, c_u32, c_vp, c_vp]),
     "ephdc_classify_host": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_u32, c_vp]),
     "ephdc_decrypt_scores": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
+    "ephdc_sr_encrypt_queries": (c_st, [c_vp, c_vp, c_vp, c_vp, c_u32, c_u32, c_u64, c_vp, c_vp]),
+    "ephdc_sr_model_plaintexts": (c_st, [c_vp, c_vp, c_vp]),
+    "ephdc_sr_evaluate": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ephdc_scores_message_bytes": (ctypes.c_size_t, [c_vp, c_u32]),
     "ephdc_pack_scores": (c_st, [c_vp, c_vp, c_u32, c_vp, c_vp]),
     "ephdc_unpack_scores": (c_st, [c_vp, c_vp, c_u32, c_vp]),

@@ -313,7 +313,25 @@ ephdc_status ephdc_keygen(const ephdc_ctx *c, uint64_t seed, ephdc_sk **out) {
     return EPHDC_OK;
 }
 
-void ephdc_sk_free(ephdc_sk *sk) { delete sk; }
+void ephdc_sk_free(ephdc_sk *sk) {
+    if (!sk) return;
+    if (sk->d_shat_mont) {
+        cudaSetDevice(sk->ctx->device);
+        cudaFree(sk->d_shat_mont);
+    }
+    delete sk;
+}
+
+// s_hat * 2^64 mod q_j on the host ([L][N]): mont_mul(a, this) = a * s_hat
+static std::vector<uint64_t> shat_mont_host(const ephdc_ctx *c, const ephdc_sk *sk) {
+    const uint32_t N = c->N, L = c->L;
+    std::vector<uint64_t> shm((size_t)L * N);
+    for (uint32_t j = 0; j < L; ++j) {
+        const uint64_t r = (uint64_t)(((u128)1 << 64) % c->q[j]);
+        for (uint32_t i = 0; i < N; ++i) shm[(size_t)j * N + i] = mulmod(sk->s_hat[(size_t)j * N + i], r, c->q[j]);
+    }
+    return shm;
+}
 
 ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_out) {
     if (!sk || !s_out) return EPHDC_ENULL;
@@ -346,11 +364,7 @@ ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const i
     m->D = D;
     if (dev_alloc(&m->d_ct, (size_t)D * L * 2 * N) != cudaSuccess) return EPHDC_ERESOURCE;
     // s_hat in Montgomery form (s_hat * 2^64 mod q): mont_mul(a, s_hat*2^64) = a * s_hat
-    std::vector<uint64_t> shm((size_t)L * N);
-    for (uint32_t j = 0; j < L; ++j) {
-        const uint64_t r = (uint64_t)(((u128)1 << 64) % c->q[j]);
-        for (uint32_t i = 0; i < N; ++i) shm[(size_t)j * N + i] = mulmod(sk->s_hat[(size_t)j * N + i], r, c->q[j]);
-    }
+    const std::vector<uint64_t> shm = shat_mont_host(c, sk);
     const uint32_t chunk = std::min<uint32_t>(D, 2048);
     DevBuf bC, bS, bM;
     if (cudaMalloc(&bC.p, (size_t)k * D) != cudaSuccess || cudaMalloc(&bS.p, sizeof(uint64_t) * shm.size()) != cudaSuccess ||
@@ -362,7 +376,8 @@ ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const i
     for (uint32_t d0 = 0; d0 < D; d0 += chunk) {
         const uint32_t nd = std::min(chunk, D - d0);
         EPHDC_CUDA_TRY(launch_pack_intt_model(c, (const int8_t *)bC.p, d0, nd, (uint32_t *)bM.p, st));
-        EPHDC_CUDA_TRY(launch_encrypt(c, (const uint32_t *)bM.p, d0, nd, (const uint64_t *)bS.p, seed, m->d_ct, st));
+        EPHDC_CUDA_TRY(launch_encrypt(c, (const uint32_t *)bM.p, d0, nd, (const uint64_t *)bS.p, seed,
+                                      m->d_ct + (size_t)d0 * L * 2 * N, st));
     }
     // FP64 path: keep the residues as exact doubles (the fused kernel's operand format)
     if (c->f64.enabled) EPHDC_CUDA_TRY(launch_u64_to_f64(m->d_ct, (size_t)D * L * 2 * N, st));
@@ -615,6 +630,57 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *c, const ephdc_model *m, ephdc
     if (s != EPHDC_OK) return s;
     EPHDC_CUDA_TRY(cudaMemcpyAsync(h_out, ws->d_out, sizeof(uint64_t) * 2 * c->L * c->N * nb, cudaMemcpyDeviceToHost, st));
     EPHDC_CUDA_TRY(cudaStreamSynchronize(st));
+    return EPHDC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// HE-HDC-SR, the server-side SIMD baseline
+// ------------------------------------------------------------------------------------
+ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *c, ephdc_sk *sk, ephdc_workspace *ws, const int8_t *d_H,
+                                      uint32_t nq, uint32_t b, uint64_t seed, uint64_t *d_qct, void *stream) {
+    if (!c || !sk || !ws || !d_H || !d_qct) return EPHDC_ENULL;
+    if (sk->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    if ((uint64_t)b * c->B >= nq) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!sk->d_shat_mont) {
+        const std::vector<uint64_t> shm = shat_mont_host(c, sk);
+        if (dev_alloc(&sk->d_shat_mont, shm.size()) != cudaSuccess) return EPHDC_ERESOURCE;
+        EPHDC_CUDA_TRY(cudaMemcpy(sk->d_shat_mont, shm.data(), sizeof(uint64_t) * shm.size(), cudaMemcpyHostToDevice));
+    }
+    const uint32_t D = c->p.D_live;
+    EPHDC_CUDA_TRY(launch_pack_intt_sr(c, d_H, false, nq, b, 0, D, ws->d_M, st));
+    EPHDC_CUDA_TRY(launch_encrypt(c, ws->d_M, b * D, D, sk->d_shat_mont, seed, d_qct, st));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_sr_model_plaintexts(const ephdc_ctx *c, const int8_t *h_class_hv, uint64_t *d_pt) {
+    if (!c || !h_class_hv || !d_pt) return EPHDC_ENULL;
+    if (c->device < 0) return EPHDC_ECONTEXT;
+    const uint32_t N = c->N, D = c->p.D_live, k = c->p.k;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    const uint32_t chunk = std::min<uint32_t>(D, 2048);
+    DevBuf bC, bM;
+    if (cudaMalloc(&bC.p, (size_t)k * D) != cudaSuccess || cudaMalloc(&bM.p, sizeof(uint32_t) * (size_t)chunk * N) != cudaSuccess)
+        return EPHDC_ERESOURCE;
+    EPHDC_CUDA_TRY(cudaMemcpy(bC.p, h_class_hv, (size_t)k * D, cudaMemcpyHostToDevice));
+    for (uint32_t d0 = 0; d0 < D; d0 += chunk) {
+        const uint32_t nd = std::min(chunk, D - d0);
+        EPHDC_CUDA_TRY(launch_pack_intt_sr(c, (const int8_t *)bC.p, true, 0, 0, d0, nd, (uint32_t *)bM.p, 0));
+        uint64_t *out = d_pt + (size_t)d0 * c->L * N;
+        if (c->f64.enabled) EPHDC_CUDA_TRY(launch_plaintext_ntt_f64(c, (const uint32_t *)bM.p, nd, out, 0));
+        else EPHDC_CUDA_TRY(launch_plaintext_ntt(c, (const uint32_t *)bM.p, nd, out, 0));
+    }
+    EPHDC_CUDA_TRY(cudaDeviceSynchronize());
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_sr_evaluate(const ephdc_ctx *c, const uint64_t *d_pt, const uint64_t *d_qct, uint64_t *d_out,
+                               void *stream) {
+    if (!c || !d_pt || !d_qct || !d_out) return EPHDC_ENULL;
+    if (c->device < 0) return EPHDC_ECONTEXT;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    EPHDC_CUDA_TRY(launch_mac_ctx(c, d_qct, d_pt, c->p.D_live, d_out, (cudaStream_t)stream));
     return EPHDC_OK;
 }
 

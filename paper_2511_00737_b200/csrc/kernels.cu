@@ -107,7 +107,7 @@ struct PackArgs {
     const TwPair<u32> *itw;
 };
 
-template <int LG, bool MODEL>
+template <int LG, bool MODEL, bool CENTER>
 __global__ void __launch_bounds__((1 << LG) / kE)
     k_pack_intt(const int8_t *__restrict__ src, u32 nq, u32 b, u32 d0, PackArgs a, u32 *__restrict__ M) {
     constexpr int N = 1 << LG, NT = N / kE;
@@ -140,9 +140,10 @@ __global__ void __launch_bounds__((1 << LG) / kE)
     for (int e = 0; e < kE; ++e) {
         const int pos = threadIdx.x + e * NT;
         const u32 y = csub(mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t), t);
-        // model plaintexts stay in [0, t) (Delta * m, reading #4); query plaintexts are
-        // stored as their centered lift (reading #3), a signed int32 (|m| < t/2 < 2^29)
-        if constexpr (MODEL) out[pos] = y;
+        // encryption inputs stay in [0, t) (Delta * m, reading #4); plaintexts that are
+        // multiplied into ciphertexts are stored as their centered lift (reading #3), a
+        // signed int32 (|m| < t/2 < 2^29)
+        if constexpr (!CENTER) out[pos] = y;
         else out[pos] = y <= half_t ? y : (u32)((int)y - (int)t);
     }
 }
@@ -362,14 +363,14 @@ struct EncArgs {
 
 template <int LG>
 __global__ void __launch_bounds__((1 << LG) / kE)
-    k_encrypt(const u32 *__restrict__ M, u32 d0, EncArgs a, u64 *__restrict__ model) {
+    k_encrypt(const u32 *__restrict__ M, u32 g0, EncArgs a, u64 *__restrict__ out) {
     constexpr int N = 1 << LG, NT = N / kE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
     __shared__ u64 cdt[ephdc_rng::kCdtLen];
     if (threadIdx.x < ephdc_rng::kCdtLen) cdt[threadIdx.x] = a.cdt[threadIdx.x];
     __syncthreads();
-    const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L, d = d0 + dd;
+    const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L, d = g0 + dd;   // d: random-stream index
     const u64 q = a.ps.q[j], delta = a.ps.delta[j], delta_p = a.ps.delta_p[j];
     const u32 *m = M + (size_t)dd * N;
     const u64 seed = a.seed;
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__((1 << LG) / kE)
         return e >= 0 ? x + (u64)e : x + q - (u64)(-e);                     // [0, 4q)
     };
     fwd_ntt<u64, LG, kE>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
-    u64 *c0 = model + (((size_t)d * a.L + j) * 2) * N;
+    u64 *c0 = out + (((size_t)dd * a.L + j) * 2) * N;
     u64 *c1 = c0 + N;
     const u64 *sh = a.shat_mont + (size_t)j * N;
     const u64 mask = a.ps.mask[j];
@@ -574,28 +575,28 @@ static PackArgs pack_args(const ephdc_ctx *c) {
     return a;
 }
 
-template <int LG, bool MODEL>
+template <int LG, bool MODEL, bool CENTER>
 static cudaError_t pack_launch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 nbat, u32 d0, u32 nd, u32 *M,
                                cudaStream_t st) {
     const size_t smem = sizeof(u32) * padded_len(1 << LG);
-    auto kern = k_pack_intt<LG, MODEL>;
+    auto kern = k_pack_intt<LG, MODEL, CENTER>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<dim3(nd, nbat), (1 << LG) / kE, smem, st>>>(src, nq, b, d0, pack_args(c), M);
     return counted(cudaGetLastError());
 }
 
-template <bool MODEL>
+template <bool MODEL, bool CENTER>
 static cudaError_t pack_dispatch(const ephdc_ctx *c, const int8_t *src, u32 nq, u32 b, u32 nbat, u32 d0, u32 nd,
                                  u32 *M, cudaStream_t st) {
     if (nd == 0 || nbat == 0) return cudaSuccess;
     if (nbat > 65535) return cudaErrorInvalidConfiguration;
     switch (c->p.log2N) {
-        case 10: return pack_launch<10, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
-        case 11: return pack_launch<11, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
-        case 12: return pack_launch<12, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
-        case 13: return pack_launch<13, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
-        case 14: return pack_launch<14, MODEL>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 10: return pack_launch<10, MODEL, CENTER>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 11: return pack_launch<11, MODEL, CENTER>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 12: return pack_launch<12, MODEL, CENTER>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 13: return pack_launch<13, MODEL, CENTER>(c, src, nq, b, nbat, d0, nd, M, st);
+        case 14: return pack_launch<14, MODEL, CENTER>(c, src, nq, b, nbat, d0, nd, M, st);
     }
     return cudaErrorInvalidValue;
 }
@@ -629,12 +630,19 @@ cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint
         }
         return cudaErrorInvalidValue;
     }
-    return pack_dispatch<false>(c, d_H, nq, b, nbat, d0, nd, d_M, st);
+    return pack_dispatch<false, true>(c, d_H, nq, b, nbat, d0, nd, d_M, st);
 }
 
 cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
                                    cudaStream_t st) {
-    return pack_dispatch<true>(c, d_C, 0, 0, 1, d0, nd, d_M, st);
+    return pack_dispatch<true, false>(c, d_C, 0, 0, 1, d0, nd, d_M, st);
+}
+
+cudaError_t launch_pack_intt_sr(const ephdc_ctx *c, const int8_t *src, bool model, uint32_t nq, uint32_t b,
+                                uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st) {
+    // HE-HDC-SR: query plaintexts to encrypt ([0, t)), class tiles to multiply (centered)
+    return model ? pack_dispatch<true, true>(c, src, 0, 0, 1, d0, nd, d_M, st)
+                 : pack_dispatch<false, false>(c, src, nq, b, 1, d0, nd, d_M, st);
 }
 
 static MacArgs mac_args(const ephdc_ctx *c) {
@@ -828,6 +836,27 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
     // reuse k_finalize with the [j][c][i] layout: prime index = i / (2N)
     k_finalize<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
     return counted(cudaGetLastError());
+}
+
+// MAC of D ciphertexts [D][L][2][N] with D plaintexts [D][L][N] under a context's primes,
+// output [2][L][N] (the scores-ciphertext layout); d_tmp: [L][2][N] scratch.
+cudaError_t launch_mac_ctx(const ephdc_ctx *c, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D, uint64_t *d_out,
+                           cudaStream_t st) {
+    ephdc_ntt_plan p;   // only the fields launch_mac reads
+    p.q = c->q;
+    p.L = c->L;
+    p.N = c->N;
+    p.log2N = c->p.log2N;
+    p.ps = c->ps;
+    u64 *tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&tmp), sizeof(u64) * 2 * c->L * c->N, st);
+    if (e != cudaSuccess) return e;
+    e = launch_mac(&p, d_ct, d_pt, D, tmp, st);
+    for (u32 cc = 0; cc < 2 && e == cudaSuccess; ++cc)   // [L][2][N] -> [2][L][N]
+        e = cudaMemcpy2DAsync(d_out + (size_t)cc * c->L * c->N, sizeof(u64) * c->N, tmp + (size_t)cc * c->N,
+                              sizeof(u64) * 2 * c->N, sizeof(u64) * c->N, c->L, cudaMemcpyDeviceToDevice, st);
+    cudaError_t e2 = cudaFreeAsync(tmp, st);
+    return e != cudaSuccess ? e : e2;
 }
 
 }  // namespace ephdc
