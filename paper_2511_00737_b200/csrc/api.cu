@@ -1,6 +1,7 @@
 // api.cu -- implementation of the C ABI declared in include/ephdc.h.
 #include <cuda_runtime.h>
 #include <string.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <memory>
@@ -219,6 +220,7 @@ ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out
         const bool ok = plan_f64(c->q, p->t, p->log2N, &c->f64);
         if (!ok && p->arith == EPHDC_ARITH_F64) return EPHDC_EPARAM;
     }
+    if (const char *e = getenv("EPHDC_F64_FLAGS")) c->f64_flags_env = (uint32_t)strtoul(e, nullptr, 0);
     c->device = device;
     if (device >= 0) {
         int ndev = 0;

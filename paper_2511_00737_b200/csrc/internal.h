@@ -71,6 +71,7 @@ struct ephdc_ctx {
     ephdc::ctxDev dev;
     uint32_t fused_S = 1, fused_chunks = 1, fused_G = 1;
     ephdc::F64Plan f64;
+    uint32_t f64_flags_env = 0;    // EPHDC_F64_FLAGS (profiling knobs, read at ctx creation)
     std::vector<uint32_t> qbits;   // bit_length(q_j): scores-message packing widths
 };
 

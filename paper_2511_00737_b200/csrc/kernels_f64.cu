@@ -62,11 +62,11 @@ template <int LGC, int S> constexpr size_t mac_f64_smem() {
            sizeof(uint32_t) * nc * S;
 }
 
-template <int LGC, int S>
+template <int LGC, int S, int WL>
 __global__ void EPHDC_F64_BOUNDS(LGC)
     k_ntt_mac_f64(const u32 *__restrict__ M, const double *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
     using namespace ephdc_async;
-    constexpr int NC = 1 << LGC, NT = NC / kE, N = NC * S;
+    constexpr int NC = 1 << LGC, N = NC * S;
     constexpr uint32_t kCols = tmem_cols<LGC>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint32_t tmem_slot;
@@ -123,7 +123,7 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
             uint32_t t[16];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const double2 w = twg[tail_twiddle_index<LGC, S>((int)s, tid + (4 * h + k) * NT)];
+                const double2 w = twg[tail_twiddle_index<LGC, S>((int)s, tail_pair<LGC, WL == 2>(4 * h + k))];
                 t[4 * k] = (uint32_t)__double2loint(w.x);
                 t[4 * k + 1] = (uint32_t)__double2hiint(w.x);
                 t[4 * k + 2] = (uint32_t)__double2loint(w.y);
@@ -169,7 +169,7 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         auto load_block = [&](int c, double2 (&dst)[4]) {
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
-                const int g = tid + (2 * c + uu) * NT;
+                const int g = tail_pair<LGC, WL == 2>(2 * c + uu);
                 dst[2 * uu] = ld_pair(c0 + 2 * g);
                 dst[2 * uu + 1] = ld_pair(c1 + 2 * g);
             }
@@ -178,7 +178,7 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
             load_block(0, mc[0]);
             load_block(1, mc[1]);
         };
-        fwd_ntt_head<LGC>(buf, load, tw, nq, after_first, before_last);
+        fwd_ntt_head<LGC, WL>(buf, load, tw, nq, after_first, before_last);
         // last stage + MAC, one 16-column TMEM block (two coefficient pairs) at a time
         const bool red = ++since_red >= a.red_every;
         if (red) since_red = 0;
@@ -195,7 +195,7 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
                 double x0, x1;
-                fwd_ntt_tail<LGC>(buf, 2 * c + uu, __hiloint2double(t[4 * uu + 1], t[4 * uu]),
+                fwd_ntt_tail<LGC, WL == 2>(buf, 2 * c + uu, __hiloint2double(t[4 * uu + 1], t[4 * uu]),
                                   __hiloint2double(t[4 * uu + 3], t[4 * uu + 2]), nq, x0, x1);
                 const double2 m0v = mc[c][2 * uu], m1v = mc[c][2 * uu + 1];
                 uint32_t *w = &r[uu * 8];
@@ -235,7 +235,7 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         u64 *o1 = out + (((size_t)b * 2 + 1) * a.L + j) * N + (size_t)s * NC;
 #pragma unroll
         for (int u = 0; u < kE / 2; ++u) {
-            const int g = tid + u * NT;
+            const int g = tail_pair<LGC, WL == 2>(u);
             const uint32_t *w = &r[u >> 1][(u & 1) * 8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -260,8 +260,6 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *tw = reinterpret_cast<double2 *>(smem_raw);
     double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * NC);
-    constexpr int NT = NC / kE;
-    const int tid = threadIdx.x;
     u32 x = blockIdx.x;
     const u32 s = x % S;
     x /= S;
@@ -289,10 +287,10 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     u64 *o = pt + ((size_t)dd * a.L + j) * N + (size_t)s * NC;
 #pragma unroll
     for (int u = 0; u < kE / 2; ++u) {
-        const int g = tid + u * NT;
+        const int g = tail_pair<LGC, false>(u);
         const double2 w = tw[NC / 2 + g];
         double x0, x1;
-        fwd_ntt_tail<LGC>(buf, u, w.x, w.y, nq, x0, x1);
+        fwd_ntt_tail<LGC, false>(buf, u, w.x, w.y, nq, x0, x1);
         ulonglong2 v;
         v.x = to_canonical_u64(reduce(x0, qinv, nq), q);
         v.y = to_canonical_u64(reduce(x1, qinv, nq), q);
@@ -423,14 +421,16 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
                                   cudaStream_t st) {
     // pad shared memory so that no more CTAs share an SM than its TMEM holds
     const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
-    auto kern = k_ntt_mac_f64<LGC, S>;
+    // experiment knob EPHDC_F64_FLAGS bits 1-2: synchronisation variant (fwd_ntt_head WL)
+    const u32 mode = (c->f64_flags_env >> 1) & 3u;
+    auto kern = mode == 1 ? k_ntt_mac_f64<LGC, S, 0> : mode == 2 ? k_ntt_mac_f64<LGC, S, 2> : k_ntt_mac_f64<LGC, S, 1>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
     F64MacArgs a = f64_args(c);
     a.nb = nb;
     f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
     // experiment knobs (profiling only; defaults are the tuned plan)
-    if (const char *e = getenv("EPHDC_F64_FLAGS")) a.flags = (u32)strtoul(e, nullptr, 0);
+    a.flags = c->f64_flags_env;
     if (const char *e = getenv("EPHDC_F64_BG")) a.bg = std::max<u32>(1, std::min<u32>(nb, (u32)strtoul(e, nullptr, 0)));
     const uint64_t groups = (nb + a.bg - 1) / a.bg;
     const uint64_t grid = groups * a.chunks * a.bg * c->L * S;

@@ -28,7 +28,14 @@ constexpr int kE = 16;  // elements per thread
 
 // One pass of R = 2^R_LOG local stages with half-sizes 2^T0_LOG ... 2^(T0_LOG-R_LOG+1).
 // (LGC - 1 - T0_LOG is a multiple of 4: pass k starts at local stage level 4k.)
-template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+// A radix-16 pass whose blocks span <= 512 elements (T0_LOG <= 8) keeps every warp
+// inside the window [512w, 512w + 512) of the buffer: if the next pass (or the tail,
+// see fwd_ntt_tail) is warp-local too, the pass needs only __syncwarp().
+template <int LGC, int T0_LOG, int R_LOG> constexpr bool warp_local_pass() {
+    return R_LOG == 4 && T0_LOG <= 8 && ((1 << LGC) / kE) % 32 == 0;
+}
+
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, bool SYNC_WARP, class Load>
 EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double nq) {
     constexpr int R = 1 << R_LOG;
     constexpr int TL_LOG = T0_LOG - (R_LOG - 1);
@@ -60,21 +67,27 @@ EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double n
 #pragma unroll
         for (int k = 0; k < R; ++k) buf[pad(base + k * TL)] = x[k];
     }
-    __syncthreads();
+    if constexpr (SYNC_WARP) __syncwarp();
+    else __syncthreads();
 }
 
 // Stages with half-sizes 2^(REM-1) ... 2^1 in passes of <= 4; the first reads from
 // load().  Hooks: before_last() runs before the last of these passes, after_first()
 // right after the first (behind its barrier: every thread has consumed load()).
-template <int LGC, int REM, bool FIRST, class Load, class H1, class H2>
+template <int LGC, int REM, bool FIRST, int WL, class Load, class H1, class H2>
 EPHDC_D void fwd_passes(double *buf, const Load &load, const double2 *tw, double nq, const H1 &after_first,
                         const H2 &before_last) {
     if constexpr (REM > 1) {
         constexpr int R_LOG = (REM - 1) >= 4 ? 4 : (REM - 1);
-        if constexpr (REM - R_LOG <= 1) before_last();
-        fwd_pass<LGC, REM - 1, R_LOG, FIRST>(buf, load, tw, nq);
+        constexpr int NEXT_REM = REM - R_LOG;
+        constexpr int NEXT_R = (NEXT_REM - 1) >= 4 ? 4 : (NEXT_REM - 1);
+        // the tail (NEXT_REM == 1) is warp-local with the windowed pair mapping (WL == 2)
+        constexpr bool next_local = NEXT_REM <= 1 ? WL == 2 : warp_local_pass<LGC, NEXT_REM - 1, NEXT_R>();
+        constexpr bool sync_warp = WL != 0 && warp_local_pass<LGC, REM - 1, R_LOG>() && next_local;
+        if constexpr (NEXT_REM <= 1) before_last();
+        fwd_pass<LGC, REM - 1, R_LOG, FIRST, sync_warp>(buf, load, tw, nq);
         if constexpr (FIRST) after_first();
-        fwd_passes<LGC, REM - R_LOG, false>(buf, load, tw, nq, after_first, before_last);
+        fwd_passes<LGC, NEXT_REM, false, WL>(buf, load, tw, nq, after_first, before_last);
     }
 }
 
@@ -105,22 +118,32 @@ template <int LGC, int S> EPHDC_D int tail_twiddle_index(int s, int g) {
 
 // All stages but the last (half-sizes NC/2 ... 2) of the forward NTT of the NC =
 // 2^LGC values load(i).  Values stay signed and lazy; DESIGN.md gives their bounds.
-template <int LGC, class Load, class H1, class H2>
+// WL: 0 = a CTA barrier after every pass; 1 = __syncwarp between warp-local head
+// passes (default: measured fastest, profiles/r01/ab_sync.txt); 2 = also before the
+// tail (windowed pair mapping -- fewer barriers, but slower model-load pattern).
+template <int LGC, int WL = 1, class Load, class H1, class H2>
 EPHDC_D void fwd_ntt_head(double *buf, const Load &load, const double2 *tw, double nq, const H1 &after_first,
                           const H2 &before_last) {
     static_assert(LGC >= 5, "at least one radix-16 pass before the final stage");
-    fwd_passes<LGC, LGC, true>(buf, load, tw, nq, after_first, before_last);
+    fwd_passes<LGC, LGC, true, WL>(buf, load, tw, nq, after_first, before_last);
 }
 
-// Last stage (half-size 1) for the coefficient pair (2g, 2g+1), g = threadIdx.x + u*NT,
-// with its twiddle (w, w/q): consecutive threads own consecutive 16-byte pairs, so the
-// caller's global accesses coalesce.  Output order: the CTA's local bit-reversed order.
-template <int LGC>
+// Pair index of the last stage.  WINDOWED: thread (warp w, lane l) owns the pairs
+// (2p, 2p+1), p = 256w + l + 32u (u < 8), inside its own warp's window [512w, 512w+512)
+// (so a warp-local last head pass needs no CTA barrier); natural: p = tid + u*NT.
+// Either way the lanes of a warp own consecutive 16-byte pairs (coalesced accesses).
+template <int LGC, bool WINDOWED> EPHDC_D int tail_pair(int u) {
+    if constexpr (WINDOWED) return (threadIdx.x >> 5) * 256 + (threadIdx.x & 31) + 32 * u;
+    else return threadIdx.x + u * ((1 << LGC) / kE);
+}
+
+// Last stage (half-size 1) for the coefficient pair p = tail_pair(u) with its twiddle
+// (w, w/q).  Output order: the CTA's local bit-reversed evaluation order.
+template <int LGC, bool WINDOWED>
 EPHDC_D void fwd_ntt_tail(const double *buf, int u, double w, double wq, double nq, double &x0, double &x1) {
-    constexpr int NT = (1 << LGC) / kE;
-    const int g = threadIdx.x + u * NT;
-    x0 = buf[pad(2 * g)];
-    x1 = buf[pad(2 * g + 1)];
+    const int p = tail_pair<LGC, WINDOWED>(u);
+    x0 = buf[pad(2 * p)];
+    x1 = buf[pad(2 * p + 1)];
     ct_bfly(x0, x1, w, wq, nq);
 }
 
