@@ -817,6 +817,9 @@ void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
         cudaFree(p->tw);
         cudaFree(p->itw);
         cudaFree(p->ninv);
+        cudaFree(p->tw_f64);
+        cudaFree(p->itw_f64);
+        cudaFree(p->ninv_f64);
     }
     delete p;
 }
@@ -851,6 +854,37 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
         ninv[2 * j] = invmod(N % q[j], q[j]);
         ninv[2 * j + 1] = shoup64(ninv[2 * j], q[j]);
     }
+    plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64);
+    if (const char *e = getenv("EPHDC_NTT_INT")) {  // profiling knob: force the integer kernels
+        if (atoi(e)) p->fwd_f64 = p->inv_f64 = false;
+    }
+    if (p->fwd_f64 || p->inv_f64) {
+        std::vector<double> f((size_t)L * N * 2), g((size_t)L * N * 2), ni(2 * L);
+        for (uint32_t j = 0; j < L; ++j) {
+            const double qd = (double)q[j];
+            for (uint32_t i = 0; i < N; ++i) {
+                const size_t k = (size_t)j * N + i;
+                f[2 * k] = i ? (double)tw[k].w : qd;
+                f[2 * k + 1] = i ? (double)tw[k].w / qd : 1.0 / qd;
+                g[2 * k] = i ? (double)itw[k].w : qd;
+                g[2 * k + 1] = i ? (double)itw[k].w / qd : 1.0 / qd;
+            }
+            ni[2 * j] = (double)ninv[2 * j];
+            ni[2 * j + 1] = (double)ninv[2 * j] / qd;
+        }
+        if (cudaMalloc(&p->tw_f64, sizeof(double) * f.size()) != cudaSuccess ||
+            cudaMalloc(&p->itw_f64, sizeof(double) * g.size()) != cudaSuccess ||
+            cudaMalloc(&p->ninv_f64, sizeof(double) * ni.size()) != cudaSuccess) {
+            ephdc_ntt_plan_free(p.release());
+            return EPHDC_ERESOURCE;
+        }
+        if (cudaMemcpy(p->tw_f64, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(p->itw_f64, g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(p->ninv_f64, ni.data(), sizeof(double) * ni.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            ephdc_ntt_plan_free(p.release());
+            return EPHDC_ECUDA;
+        }
+    }
     if (dev_alloc(&p->tw, tw.size()) != cudaSuccess || dev_alloc(&p->itw, itw.size()) != cudaSuccess ||
         dev_alloc(&p->ninv, ninv.size()) != cudaSuccess) {
         ephdc_ntt_plan_free(p.release());
@@ -869,14 +903,18 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
 ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, false, (cudaStream_t)stream));
+    const cudaError_t e = launch_ntt_batch_f64(p, d_polys, batch, false, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, false, (cudaStream_t)stream));
+    else EPHDC_CUDA_TRY(e);
     return EPHDC_OK;
 }
 
 ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, true, (cudaStream_t)stream));
+    const cudaError_t e = launch_ntt_batch_f64(p, d_polys, batch, true, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, true, (cudaStream_t)stream));
+    else EPHDC_CUDA_TRY(e);
     return EPHDC_OK;
 }
 

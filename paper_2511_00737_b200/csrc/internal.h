@@ -115,6 +115,10 @@ struct ephdc_ntt_plan {
     ephdc::PrimeSet ps{};
     TwPair<u64> *tw = nullptr, *itw = nullptr;  // [L][N]
     uint64_t *ninv = nullptr;                            // [L][2] (N^-1, Shoup)
+    // FP64 path (kernels_f64.cu k_ntt_std_f64) when the bounds allow it
+    bool fwd_f64 = false, inv_f64 = false;
+    double2 *tw_f64 = nullptr, *itw_f64 = nullptr;       // [L][N] (w, w/q); entry 0 = (q, 1/q)
+    double2 *ninv_f64 = nullptr;                         // [L] (N^-1, N^-1/q)
 };
 
 namespace ephdc {
@@ -170,6 +174,14 @@ cudaError_t launch_plaintext_ntt_f64(const ephdc_ctx *c, const uint32_t *d_M, ui
                                      cudaStream_t st);
 cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, cudaStream_t st);
 int ntt_mac_f64_occupancy(uint32_t log2N);
+struct StdF64Args {
+    u32 L;
+    const double2 *tw;     // [L][N] forward or inverse (w, w/q); entry 0 = (q, 1/q)
+    const double2 *ninv;   // [L] (N^-1, N^-1/q)
+};
+cudaError_t launch_ntt_batch_f64(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t batch, bool inverse,
+                                 cudaStream_t st);
+void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv);
 bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan);
 void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G);
 int ntt_mac_occupancy(uint32_t log2N, uint32_t S);

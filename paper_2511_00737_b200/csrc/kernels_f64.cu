@@ -298,6 +298,173 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     }
 }
 
+// =====================================================================================
+// Standalone negacyclic NTT on the FP64 pipe (c5 microbench; primes within the bounds
+// of ephdc_ntt_plan_create).  In place on [batch][L][N] canonical u64.  CTA = (poly,
+// prime, slice s of S = N/NC); forward at N = 2^14 runs as a 2-CTA cluster: each CTA
+// computes the first stage for its output half while loading both halves, and a
+// cluster barrier after the first pass keeps either CTA from overwriting input its
+// partner still reads.  Inverse: S = 1 (N <= 2^13).
+// =====================================================================================
+template <int LGC, int S, bool INV>
+__global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restrict__ polys, u32 batch, StdF64Args a) {
+    constexpr int NC = 1 << LGC, N = NC * S;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *tw = reinterpret_cast<double2 *>(smem_raw);
+    double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * NC);
+    const int tid = threadIdx.x;
+    // persistent: CTA (worker w, prime j, slice s) transforms polys b = w, w + W, ... of prime j
+    const u32 s = blockIdx.x % S, wj = blockIdx.x / S, j = wj % a.L, w0 = wj / a.L;
+    const u32 W = gridDim.x / (S * a.L);
+    const double2 *twg = a.tw + (size_t)j * N;
+    const double2 qq = twg[0];
+    const double q = qq.x, nq = -q, qinv = qq.y, half_q = 0.5 * q;
+    if constexpr (INV) load_inv_twiddles<LGC>(tw, twg);
+    else load_twiddles<LGC, S>(tw, twg, (int)s, NC);
+    double2 w1 = make_double2(0.0, 0.0);
+    if constexpr (S > 1) w1 = twg[1];
+    const double2 ni = INV ? a.ninv[j] : make_double2(0.0, 0.0);
+    __syncthreads();
+    auto centered = [&](u64 v) -> double {   // [0, q) -> (-q/2, q/2]
+        const double x = from_u64(v);
+        return x > half_q ? __dsub_rn(x, q) : x;
+    };
+    for (u32 b = w0; b < batch; b += W) {
+        u64 *p = polys + ((size_t)b * a.L + j) * N;
+        if (b + W < batch) {   // next polynomial of this CTA into L2 while this one computes
+            const u64 *pn = polys + ((size_t)(b + W) * a.L + j) * N + (size_t)s * NC;
+            for (int l = tid; l < (NC * 8) / 128; l += NC / kE) prefetch_l2(pn + 16 * l);
+        }
+        if constexpr (!INV) {
+            auto load = [&](int pos) -> double {
+                const double U = centered(__ldcs(reinterpret_cast<const unsigned long long *>(p + pos)));
+                if constexpr (S == 1) {
+                    return U;
+                } else {
+                    const double V = centered(__ldcs(reinterpret_cast<const unsigned long long *>(p + pos + NC)));
+                    const double T = mul_tw(V, w1.x, w1.y, nq);
+                    return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
+                }
+            };
+            auto after_first = [&]() {   // both halves consumed by both CTAs before any store
+                if constexpr (S > 1) {
+                    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+                    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+                }
+            };
+            auto none = [] {};
+            fwd_ntt_head<LGC>(buf, load, tw, nq, after_first, none);
+            u64 *o = p + (size_t)s * NC;
+#pragma unroll
+            for (int u = 0; u < kE / 2; ++u) {
+                const int g = tail_pair<LGC, false>(u);
+                const double2 w = tw[NC / 2 + g];
+                double x0, x1;
+                fwd_ntt_tail<LGC, false>(buf, u, w.x, w.y, nq, x0, x1);
+                ulonglong2 v;
+                v.x = to_canonical_u64(reduce(x0, qinv, nq), q);
+                v.y = to_canonical_u64(reduce(x1, qinv, nq), q);
+                __stcs(reinterpret_cast<ulonglong2 *>(o + 2 * g), v);
+            }
+        } else {
+            auto load = [&](int pos) -> double {
+                return centered(__ldcs(reinterpret_cast<const unsigned long long *>(p + pos)));
+            };
+            inv_ntt_f64<LGC, 0, true>(buf, load, tw, nq);
+            constexpr int NT = NC / kE;
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                const int pos = tid + e * NT;
+                const double y = reduce(mul_tw(buf[pad(pos)], ni.x, ni.y, nq), qinv, nq);
+                __stcs(reinterpret_cast<unsigned long long *>(p + pos), (unsigned long long)to_canonical_u64(y, q));
+            }
+        }
+        __syncthreads();   // buf is rewritten by the next polynomial
+    }
+}
+
+template <int LGC, int S, bool INV>
+static cudaError_t std_f64_launch(const ephdc_ntt_plan *pl, u64 *polys, u32 batch, cudaStream_t st) {
+    const size_t smem = sizeof(double2) * ((size_t)1 << LGC) + sizeof(double) * (size_t)padded_len(1 << LGC);
+    auto kern = k_ntt_std_f64<LGC, S, INV>;
+    cudaError_t e = smem_attr(kern, smem);
+    if (e != cudaSuccess) return e;
+    StdF64Args a;
+    a.L = pl->L;
+    a.tw = INV ? pl->itw_f64 : pl->tw_f64;
+    a.ninv = pl->ninv_f64;
+    // workers per prime: fill the GPU (CTAs per SM from shared memory), at most batch
+    const int per_sm = std::max<int>(1, (int)((228u << 10) / (smem + 1024)));
+    const uint64_t ctas = 148ull * per_sm;
+    const uint64_t W = std::max<uint64_t>(1, std::min<uint64_t>(batch, ctas / ((uint64_t)pl->L * S)));
+    const uint64_t grid = W * pl->L * S;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((1 << LGC) / kE);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, polys, batch, a);
+    return counted(e == cudaSuccess ? cudaGetLastError() : e);
+}
+
+// FP64 standalone NTT if the plan allows it for this direction and size; returns
+// cudaErrorNotSupported otherwise (the caller then runs the integer kernels).
+cudaError_t launch_ntt_batch_f64(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t batch, bool inverse,
+                                 cudaStream_t st) {
+    if (inverse ? !pl->inv_f64 : !pl->fwd_f64) return cudaErrorNotSupported;
+    if (batch == 0) return cudaSuccess;
+    if (!inverse) {
+        switch (pl->log2N) {
+            case 10: return std_f64_launch<10, 1, false>(pl, d_polys, batch, st);
+            case 11: return std_f64_launch<11, 1, false>(pl, d_polys, batch, st);
+            case 12: return std_f64_launch<12, 1, false>(pl, d_polys, batch, st);
+            case 13: return std_f64_launch<13, 1, false>(pl, d_polys, batch, st);
+            case 14: return std_f64_launch<13, 2, false>(pl, d_polys, batch, st);
+        }
+    } else {
+        switch (pl->log2N) {
+            case 10: return std_f64_launch<10, 1, true>(pl, d_polys, batch, st);
+            case 11: return std_f64_launch<11, 1, true>(pl, d_polys, batch, st);
+            case 12: return std_f64_launch<12, 1, true>(pl, d_polys, batch, st);
+            case 13: return std_f64_launch<13, 1, true>(pl, d_polys, batch, st);
+        }
+    }
+    return cudaErrorNotSupported;
+}
+
+// Bounds of the standalone FP64 transforms: canonical inputs are
+// centered (|x| <= q/2); forward CT stages add <= (1/2 + B 2^-54) q each, inverse GS
+// stages double the bound; every mul_tw input must stay below 2^51.
+void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv) {
+    const double L51 = 0.98 * 2251799813685248.0, e54 = 1.0 / 18014398509481984.0;
+    *fwd = log2N >= 10 && log2N <= 14;
+    *inv = log2N >= 10 && log2N <= 13;
+    for (uint64_t qj : q) {
+        if (qj >= (1ull << 50)) {
+            *fwd = *inv = false;
+            return;
+        }
+        const double Q = (double)qj;
+        double B = Q / 2 + 1;
+        for (uint32_t st = 0; st < log2N; ++st) {
+            if (B >= L51) *fwd = false;
+            B += (0.5 + B * e54) * Q + 2.0;
+        }
+        double Bi = Q / 2 + 1;
+        for (uint32_t st = 0; st < log2N; ++st) {
+            if (2 * Bi >= L51) *inv = false;
+            Bi *= 2;
+        }
+    }
+}
+
 // model residues u64 -> exact doubles, in place (setup, once per model)
 __global__ void k_u64_to_f64(u64 *__restrict__ d, size_t n) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

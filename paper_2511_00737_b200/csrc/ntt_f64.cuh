@@ -147,4 +147,71 @@ EPHDC_D void fwd_ntt_tail(const double *buf, int u, double w, double wq, double 
     ct_bfly(x0, x1, w, wq, nq);
 }
 
+// ---------------------------------------------------------------------------------
+// Inverse (Gentleman-Sande) passes on doubles, for the standalone c5 transform.  The
+// sums X + Y double their bound every stage, so callers check 2^(LGC-1) * B0 < 2^51
+// (ephdc_ntt_plan_create).  Twiddles in shared memory in the pass-major layout: the
+// twiddle of (sub-stage sub, block-group blk, v) at slot NC/2^(T0+sub+1) + v*nblk + blk.
+// ---------------------------------------------------------------------------------
+template <int NC, int T0_LOG, int R_LOG, int SUB>
+EPHDC_D void gs_substages_f64(double (&x)[1 << R_LOG], const double2 *tw, int blk, double nq) {
+    if constexpr (SUB < R_LOG) {
+        constexpr int R = 1 << R_LOG, hs = 1 << SUB, nv = R / (2 * hs), nblk = NC >> (T0_LOG + R_LOG);
+#pragma unroll
+        for (int v = 0; v < nv; ++v) {
+            const double2 w = tw[(NC >> (T0_LOG + SUB + 1)) + v * nblk + blk];
+#pragma unroll
+            for (int kk = 0; kk < hs; ++kk) gs_bfly(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w.x, w.y, nq);
+        }
+        gs_substages_f64<NC, T0_LOG, R_LOG, SUB + 1>(x, tw, blk, nq);
+    }
+}
+
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+EPHDC_D void inv_pass_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+    constexpr int NC = 1 << LGC, NT = NC / kE, R = 1 << R_LOG, T0 = 1 << T0_LOG;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kE / R; ++u) {
+        const int g = tid + u * NT;
+        const int blk = g >> T0_LOG, off = g & (T0 - 1);
+        const int base = blk * (T0 * R) + off;
+        double x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            if constexpr (FROM_LOAD) x[k] = load(base + k * T0);
+            else x[k] = buf[pad(base + k * T0)];
+        }
+        gs_substages_f64<NC, T0_LOG, R_LOG, 0>(x, tw, blk, nq);
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
+    }
+    __syncthreads();
+}
+
+template <int LGC, int DONE, bool FIRST, class Load>
+EPHDC_D void inv_ntt_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+    if constexpr (DONE < LGC) {
+        constexpr int R_LOG = (LGC - DONE) >= 4 ? 4 : (LGC - DONE);
+        inv_pass_f64<LGC, DONE, R_LOG, FIRST>(buf, load, tw, nq);
+        inv_ntt_f64<LGC, DONE + R_LOG, false>(buf, load, tw, nq);
+    }
+}
+
+// Fills tw_s[1..NC) with the inverse twiddles psi^-1_rev of a full NC-point transform
+// in the pass-major layout of inv_pass_f64.
+template <int LGC>
+EPHDC_D void load_inv_twiddles(double2 *tw_s, const double2 *__restrict__ twg) {
+    constexpr int NC = 1 << LGC, NT = NC / kE;
+    for (int p = threadIdx.x; p < NC; p += NT) {
+        if (p == 0) continue;
+        const int lsb = 31 - __clz(p), sb = 1 << lsb;
+        const int st = LGC - 1 - lsb, done = st & ~3, sub = st - done;
+        const int rlog = (LGC - done) < 4 ? (LGC - done) : 4;
+        const int nblk = NC >> (done + rlog);
+        const int r = p - sb, v = r / nblk, blk = r % nblk;
+        tw_s[p] = twg[sb + blk * ((1 << rlog) >> (sub + 1)) + v];
+    }
+}
+
 }  // namespace ephdc_f64
