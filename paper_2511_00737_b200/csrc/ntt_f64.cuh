@@ -47,11 +47,17 @@ EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double n
         const int g = tid + u * NT;
         const int blk = g >> TL_LOG, off = g & (TL - 1);
         const int base = (blk << (T0_LOG + 1)) + off;
+        // pad(base + k*TL) = pad(base) + k*TL + (k*TL >> 4) whenever the block stride
+        // 2^(T0+1) is a multiple of 16 (off < TL never carries into the next 16): one
+        // address register plus compile-time offsets
+        constexpr bool kConstPad = T0_LOG >= 3;
+        const int pb = pad(base);
+        auto addr = [&](int k) { return kConstPad ? pb + k * TL + ((k * TL) >> 4) : pad(base + k * TL); };
         double x[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
-            else x[k] = buf[pad(base + k * TL)];
+            else x[k] = buf[addr(k)];
         }
         constexpr int m0 = (1 << LGC) >> (T0_LOG + 1);
 #pragma unroll
@@ -65,7 +71,7 @@ EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double n
             }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[pad(base + k * TL)] = x[k];
+        for (int k = 0; k < R; ++k) buf[addr(k)] = x[k];
     }
     if constexpr (SYNC_WARP) __syncwarp();
     else __syncthreads();
@@ -142,8 +148,9 @@ template <int LGC, bool WINDOWED> EPHDC_D int tail_pair(int u) {
 template <int LGC, bool WINDOWED>
 EPHDC_D void fwd_ntt_tail(const double *buf, int u, double w, double wq, double nq, double &x0, double &x1) {
     const int p = tail_pair<LGC, WINDOWED>(u);
-    x0 = buf[pad(2 * p)];
-    x1 = buf[pad(2 * p + 1)];
+    const int a = pad(2 * p);   // 2p is even: 2p + 1 stays in the same 16-word row
+    x0 = buf[a];
+    x1 = buf[a + 1];
     ct_bfly(x0, x1, w, wq, nq);
 }
 
