@@ -10,7 +10,8 @@ import os
 from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libephdc.so")
+# EPHDC_LIB: an alternative build of the same library (A/B experiments, tools/ab_libs.sh)
+LIB_PATH = os.environ.get("EPHDC_LIB") or os.path.join(HERE, "libephdc.so")
 
 MAX_PRIMES = 16
 
