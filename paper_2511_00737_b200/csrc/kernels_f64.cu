@@ -30,7 +30,19 @@ namespace {
 
 EPHDC_D void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-EPHDC_D double2 ld_pair(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
+// model residue pairs: read by every batch of a group within a few microseconds, so
+// they are loaded (and prefetched) with an L2 evict_last policy
+EPHDC_D uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+EPHDC_D double2 ld_pair(const double *p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+EPHDC_D void prefetch_l2_last(const void *p) { asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p)); }
 
 inline cudaError_t counted(cudaError_t e) {
     if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -134,12 +146,13 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     }
 
     u32 since_red = 0, phase = 0;
+    const uint64_t pol = l2_evict_last_policy();
     for (u32 d = d0; d < d1; ++d) {
         const double *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
         const double *c1 = c0 + N;
         if (!(a.flags & 1u)) {
-            prefetch_l2(c0 + 16 * tid);  // this dim's model slice, read by the last stage
-            prefetch_l2(c1 + 16 * tid);
+            prefetch_l2_last(c0 + 16 * tid);  // this dim's model slice, read by the last stage
+            prefetch_l2_last(c1 + 16 * tid);
         }
         mbar_wait(&mbar, phase);     // plaintext row d is in mst
         phase ^= 1u;
@@ -170,8 +183,8 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
                 const int g = tail_pair<LGC, WL == 2>(2 * c + uu);
-                dst[2 * uu] = ld_pair(c0 + 2 * g);
-                dst[2 * uu + 1] = ld_pair(c1 + 2 * g);
+                dst[2 * uu] = ld_pair(c0 + 2 * g, pol);
+                dst[2 * uu + 1] = ld_pair(c1 + 2 * g, pol);
             }
         };
         auto before_last = [&]() {

@@ -42,6 +42,37 @@ KERNEL(k_mul64hi, uint64_t, 3, asm volatile("mul.hi.u64 %0, %0, %1;" : "+l"(r[c]
 KERNEL(k_mul64lo, uint64_t, 3, asm volatile("mul.lo.u64 %0, %0, %1;" : "+l"(r[c]) : "l"((uint64_t)m * 0x9E3779B97F4A7C15ull | 1)))
 // FP64 FMA (for reference: the DFMA pipe)
 KERNEL(k_dfma, double, 1, asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(r[c]) : "d"(1.0000001)))
+KERNEL(k_dadd, double, 1, asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(r[c]) : "d"(1.0000001)))
+KERNEL(k_dmul, double, 1, asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(r[c]) : "d"(1.0000001)))
+
+// The exact FP64 Cooley-Tukey butterfly of csrc/modf64.cuh (8 FP64 instructions:
+// DMUL, 3 DFMA, 4 DADD) on CH independent (X, Y) pairs: the achievable FP64 rate of
+// the NTT's instruction mix.  Counted as 8 ops per butterfly.
+__global__ void k_bfly(double *out, unsigned long long *clk) {
+    const double q = 281474976546817.0, nq = -q, w = 23720796222.0, wq = w / q, R = 6755399441055744.0;
+    double X[CH], Y[CH];
+    for (int c = 0; c < CH; ++c) { X[c] = threadIdx.x * 7 + c; Y[c] = threadIdx.x * 3 + c * 11; }
+    unsigned long long c0 = clock64(), g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    for (int i = 0; i < ITERS / 8; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const double y = Y[c], x = X[c];
+            const double h = __dmul_rn(y, w);
+            const double l = __fma_rn(y, w, -h);
+            const double k = __dadd_rn(__fma_rn(y, wq, R), -R);
+            const double t = __dadd_rn(__fma_rn(k, nq, h), l);
+            X[c] = __dadd_rn(x, t);
+            Y[c] = __dsub_rn(x, t);
+        }
+    }
+    unsigned long long c1 = clock64(), g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    double s = 0;
+    for (int c = 0; c < CH; ++c) s += X[c] + Y[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0 && blockIdx.x == 0) { clk[0] = c1 - c0; clk[1] = g1 - g0; }
+}
 
 template <class K, class T>
 static void run(const char *name, K kern, int blocks, int threads) {
@@ -82,5 +113,10 @@ int main() {
     run<decltype(k_mul64hi), uint64_t>("mul.hi.u64", k_mul64hi, blocks, threads);
     run<decltype(k_mul64lo), uint64_t>("mul.lo.u64", k_mul64lo, blocks, threads);
     run<decltype(k_dfma), double>("DFMA(fma.rn.f64)", k_dfma, blocks, threads);
+    run<decltype(k_dadd), double>("DADD(add.rn.f64)", k_dadd, blocks, threads);
+    run<decltype(k_dmul), double>("DMUL(mul.rn.f64)", k_dmul, blocks, threads);
+    // butterfly mix: ITERS/8 iterations x CH butterflies x 8 FP64 instructions = ITERS*CH ops
+    run<decltype(k_bfly), double>("FP64 butterfly mix (8 ops/bfly), 8x256 thr/SM", k_bfly, blocks, threads);
+    run<decltype(k_bfly), double>("FP64 butterfly mix (8 ops/bfly), 1x512 thr/SM", k_bfly, sms, 512);
     return 0;
 }
