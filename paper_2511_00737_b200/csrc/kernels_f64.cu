@@ -74,12 +74,25 @@ template <int LGC, int S> constexpr size_t mac_f64_smem() {
            sizeof(uint32_t) * nc * S;
 }
 
-template <int LGC, int S, int WL>
-__global__ void EPHDC_F64_BOUNDS(LGC)
+// E = elements per thread (16: NC/16 threads x <= 128 registers; 32: NC/32 threads,
+// twice the independent work per warp, up to 255 registers).
+template <int LGC, int E> constexpr int mac_threads() { return (1 << LGC) / E; }
+template <int LGC, int E> constexpr int mac_min_blocks() { return E == kE ? f64_ctas_per_sm<LGC>() : 1; }
+
+template <int LGC, int S, int WL, int E>
+__global__ void __launch_bounds__(mac_threads<LGC, E>(), mac_min_blocks<LGC, E>())
     k_ntt_mac_f64(const u32 *__restrict__ M, const double *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
     using namespace ephdc_async;
     constexpr int NC = 1 << LGC, N = NC * S;
-    constexpr uint32_t kCols = tmem_cols<LGC>();
+    // TMEM: per thread 4E accumulator columns (E coefficients x 2 components x 2 words)
+    // and 2E last-stage twiddle columns; warps of one lane quarter split the 512 columns
+    constexpr int kWarps = NC / E / 32;
+    constexpr uint32_t kWarpCols = kWarps >= 4 ? 512u / (uint32_t)(kWarps / 4) : 512u;
+    static_assert(6 * E <= (int)kWarpCols, "TMEM columns per warp");
+    constexpr uint32_t kCols = E == kE ? tmem_cols<LGC>() : 512u;
+    constexpr uint32_t kColStride = E == kE ? 128u : kWarpCols;
+    constexpr int NBLK = E / 4;                 // tail blocks of 2 coefficient pairs
+    constexpr int PRE = E == kE ? 2 : 4;        // model blocks requested before the last head pass
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t mbar;
@@ -113,29 +126,29 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     const double2 *twg = a.tw + (size_t)j * N;
     const double2 qq = twg[0];  // slot 0 of the table holds (q_j, fl(1/q_j))
     const double q = qq.x, nq = -q, qinv = qq.y;
-    load_twiddles<LGC, S>(tw, twg, (int)s, NC / 2);
+    load_twiddles<LGC, S, E>(tw, twg, (int)s, NC / 2);
     double2 w1 = make_double2(0.0, 0.0);
     if constexpr (S > 1) w1 = twg[1];
     ephdc_tmem::fence_before_sync();
     __syncthreads();
     ephdc_tmem::fence_after_sync();
-    // this thread's TMEM columns: block c (pairs g = tid + u*NT, u = 2c, 2c+1) keeps its
+    // this thread's TMEM columns: block c (pairs tail_pair(2c), tail_pair(2c+1)) keeps its
     // accumulators at 16c .. 16c+15 = (acc0[2u], acc0[2u+1], acc1[2u], acc1[2u+1]) x 2 words
-    // and its last-stage twiddles at 64 + 8c .. 64 + 8c + 7 = (w, w/q) x 2 words x 2 pairs
-    const uint32_t tacc = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 128u;
-    const uint32_t ttw = tacc + 64u;
+    // and its last-stage twiddles at 4E + 8c .. 4E + 8c + 7 = (w, w/q) x 2 words x 2 pairs
+    const uint32_t tacc = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * kColStride;
+    const uint32_t ttw = tacc + 4u * E;
     {
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ephdc_tmem::st16(tacc + 16 * c, z);
+        for (int c = 0; c < NBLK; ++c) ephdc_tmem::st16(tacc + 16 * c, z);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < E / 8; ++h) {
             uint32_t t[16];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const double2 w = twg[tail_twiddle_index<LGC, S>((int)s, tail_pair<LGC, WL == 2>(4 * h + k))];
+                const double2 w = twg[tail_twiddle_index<LGC, S>((int)s, tail_pair<LGC, WL == 2, E>(4 * h + k))];
                 t[4 * k] = (uint32_t)__double2loint(w.x);
                 t[4 * k + 1] = (uint32_t)__double2hiint(w.x);
                 t[4 * k + 2] = (uint32_t)__double2loint(w.y);
@@ -182,24 +195,25 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
         auto load_block = [&](int c, double2 (&dst)[4]) {
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
-                const int g = tail_pair<LGC, WL == 2>(2 * c + uu);
+                const int g = tail_pair<LGC, WL == 2, E>(2 * c + uu);
                 dst[2 * uu] = ld_pair(c0 + 2 * g, pol);
                 dst[2 * uu + 1] = ld_pair(c1 + 2 * g, pol);
             }
         };
         auto before_last = [&]() {
-            load_block(0, mc[0]);
-            load_block(1, mc[1]);
+#pragma unroll
+            for (int c = 0; c < PRE; ++c) load_block(c, mc[c]);
         };
-        fwd_ntt_head<LGC, WL>(buf, load, tw, nq, after_first, before_last);
-        // last stage + MAC, one 16-column TMEM block (two coefficient pairs) at a time
+        fwd_ntt_head<LGC, WL, E>(buf, load, tw, nq, after_first, before_last);
+        // last stage + MAC, one 16-column TMEM block (two coefficient pairs) at a time;
+        // model blocks stream 4 ahead through mc[c % 4]
         const bool red = ++since_red >= a.red_every;
         if (red) since_red = 0;
         ephdc_tmem::wait_st();
-        load_block(2, mc[2]);
-        load_block(3, mc[3]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = PRE; c < 4 && c < NBLK; ++c) load_block(c, mc[c]);
+#pragma unroll
+        for (int c = 0; c < NBLK; ++c) {
             uint32_t r[16], t[8];
             ephdc_tmem::ld16(tacc + 16 * c, r);
             ephdc_tmem::ld8(ttw + 8 * c, t);
@@ -208,9 +222,9 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
                 double x0, x1;
-                fwd_ntt_tail<LGC, WL == 2>(buf, 2 * c + uu, __hiloint2double(t[4 * uu + 1], t[4 * uu]),
+                fwd_ntt_tail<LGC, WL == 2, E>(buf, 2 * c + uu, __hiloint2double(t[4 * uu + 1], t[4 * uu]),
                                   __hiloint2double(t[4 * uu + 3], t[4 * uu + 2]), nq, x0, x1);
-                const double2 m0v = mc[c][2 * uu], m1v = mc[c][2 * uu + 1];
+                const double2 m0v = mc[c % 4][2 * uu], m1v = mc[c % 4][2 * uu + 1];
                 uint32_t *w = &r[uu * 8];
                 double v[4] = {__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]),
                                __hiloint2double(w[5], w[4]), __hiloint2double(w[7], w[6])};
@@ -229,6 +243,7 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
                 }
             }
             ephdc_tmem::st16(tacc + 16 * c, r);
+            if (c + 4 < NBLK) load_block(c + 4, mc[c % 4]);
         }
         __syncthreads();  // the next first pass overwrites buf
     }
@@ -236,19 +251,18 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
     // sums of <= chunks values < q fit 64 bits (checked on the host) and integer
     // addition is order-independent, so the result is deterministic
     {
-        uint32_t r[4][16];
+        uint32_t r[NBLK][16];
         ephdc_tmem::wait_st();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ephdc_tmem::ld16(tacc + 16 * c, r[c]);
+        for (int c = 0; c < NBLK; ++c) ephdc_tmem::ld16(tacc + 16 * c, r[c]);
         ephdc_tmem::wait_ld(r[0]);
-        ephdc_tmem::after_wait(r[1]);
-        ephdc_tmem::after_wait(r[2]);
-        ephdc_tmem::after_wait(r[3]);
+#pragma unroll
+        for (int c = 1; c < NBLK; ++c) ephdc_tmem::after_wait(r[c]);
         u64 *o0 = out + (((size_t)b * 2 + 0) * a.L + j) * N + (size_t)s * NC;
         u64 *o1 = out + (((size_t)b * 2 + 1) * a.L + j) * N + (size_t)s * NC;
 #pragma unroll
-        for (int u = 0; u < kE / 2; ++u) {
-            const int g = tail_pair<LGC, WL == 2>(u);
+        for (int u = 0; u < E / 2; ++u) {
+            const int g = tail_pair<LGC, WL == 2, E>(u);
             const uint32_t *w = &r[u >> 1][(u & 1) * 8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -603,7 +617,10 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
     const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
     // experiment knob EPHDC_F64_FLAGS bits 1-2: synchronisation variant (fwd_ntt_head WL)
     const u32 mode = (c->f64_flags_env >> 1) & 3u;
-    auto kern = mode == 1 ? k_ntt_mac_f64<LGC, S, 0> : mode == 2 ? k_ntt_mac_f64<LGC, S, 2> : k_ntt_mac_f64<LGC, S, 1>;
+    // experiment knob bit 3: 32 elements per thread (LGC = 13 only)
+    const bool e32 = LGC == 13 && (c->f64_flags_env & 8u) != 0;
+    auto kern = e32 ? k_ntt_mac_f64<LGC, S, 1, 32>
+                    : mode == 1 ? k_ntt_mac_f64<LGC, S, 0, kE> : mode == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
     F64MacArgs a = f64_args(c);
@@ -615,7 +632,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
     const uint64_t groups = (nb + a.bg - 1) / a.bg;
     const uint64_t grid = groups * a.chunks * a.bg * c->L * S;
     if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-    kern<<<(unsigned)grid, (1 << LGC) / kE, smem, st>>>(M, model, out, a);
+    kern<<<(unsigned)grid, (1 << LGC) / (e32 ? 32 : kE), smem, st>>>(M, model, out, a);
     return counted(cudaGetLastError());
 }
 

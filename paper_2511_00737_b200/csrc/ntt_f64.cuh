@@ -31,19 +31,19 @@ constexpr int kE = 16;  // elements per thread
 // A radix-16 pass whose blocks span <= 512 elements (T0_LOG <= 8) keeps every warp
 // inside the window [512w, 512w + 512) of the buffer: if the next pass (or the tail,
 // see fwd_ntt_tail) is warp-local too, the pass needs only __syncwarp().
-template <int LGC, int T0_LOG, int R_LOG> constexpr bool warp_local_pass() {
-    return R_LOG == 4 && T0_LOG <= 8 && ((1 << LGC) / kE) % 32 == 0;
+template <int LGC, int T0_LOG, int R_LOG, int E = kE> constexpr bool warp_local_pass() {
+    return R_LOG == 4 && T0_LOG <= 8 && ((1 << LGC) / E) % 32 == 0;
 }
 
-template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, bool SYNC_WARP, class Load>
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, bool SYNC_WARP, int E, class Load>
 EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double nq) {
     constexpr int R = 1 << R_LOG;
     constexpr int TL_LOG = T0_LOG - (R_LOG - 1);
     constexpr int TL = 1 << TL_LOG;
-    constexpr int NT = (1 << LGC) / kE;
+    constexpr int NT = (1 << LGC) / E;
     const int tid = threadIdx.x;
 #pragma unroll
-    for (int u = 0; u < kE / R; ++u) {
+    for (int u = 0; u < E / R; ++u) {
         const int g = tid + u * NT;
         const int blk = g >> TL_LOG, off = g & (TL - 1);
         const int base = (blk << (T0_LOG + 1)) + off;
@@ -80,7 +80,7 @@ EPHDC_D void fwd_pass(double *buf, const Load &load, const double2 *tw, double n
 // Stages with half-sizes 2^(REM-1) ... 2^1 in passes of <= 4; the first reads from
 // load().  Hooks: before_last() runs before the last of these passes, after_first()
 // right after the first (behind its barrier: every thread has consumed load()).
-template <int LGC, int REM, bool FIRST, int WL, class Load, class H1, class H2>
+template <int LGC, int REM, bool FIRST, int WL, int E, class Load, class H1, class H2>
 EPHDC_D void fwd_passes(double *buf, const Load &load, const double2 *tw, double nq, const H1 &after_first,
                         const H2 &before_last) {
     if constexpr (REM > 1) {
@@ -88,21 +88,21 @@ EPHDC_D void fwd_passes(double *buf, const Load &load, const double2 *tw, double
         constexpr int NEXT_REM = REM - R_LOG;
         constexpr int NEXT_R = (NEXT_REM - 1) >= 4 ? 4 : (NEXT_REM - 1);
         // the tail (NEXT_REM == 1) is warp-local with the windowed pair mapping (WL == 2)
-        constexpr bool next_local = NEXT_REM <= 1 ? WL == 2 : warp_local_pass<LGC, NEXT_REM - 1, NEXT_R>();
-        constexpr bool sync_warp = WL != 0 && warp_local_pass<LGC, REM - 1, R_LOG>() && next_local;
+        constexpr bool next_local = NEXT_REM <= 1 ? WL == 2 : warp_local_pass<LGC, NEXT_REM - 1, NEXT_R, E>();
+        constexpr bool sync_warp = WL != 0 && warp_local_pass<LGC, REM - 1, R_LOG, E>() && next_local;
         if constexpr (NEXT_REM <= 1) before_last();
-        fwd_pass<LGC, REM - 1, R_LOG, FIRST, sync_warp>(buf, load, tw, nq);
+        fwd_pass<LGC, REM - 1, R_LOG, FIRST, sync_warp, E>(buf, load, tw, nq);
         if constexpr (FIRST) after_first();
-        fwd_passes<LGC, NEXT_REM, false, WL>(buf, load, tw, nq, after_first, before_last);
+        fwd_passes<LGC, NEXT_REM, false, WL, E>(buf, load, tw, nq, after_first, before_last);
     }
 }
 
 // Fills tw_s[1..n_slots) (n_slots = NC/2: the head stages only, or NC: also the last
 // stage) with the slice-s twiddles of a prime (twg = [N] (w, w/q) pairs in psi_rev
 // order) in the pass layout described above.  All NT threads call it.
-template <int LGC, int S>
+template <int LGC, int S, int E = kE>
 EPHDC_D void load_twiddles(double2 *tw_s, const double2 *__restrict__ twg, int s, int n_slots) {
-    constexpr int NT = (1 << LGC) / kE;
+    constexpr int NT = (1 << LGC) / E;
     for (int p = threadIdx.x; p < n_slots; p += NT) {
         if (p == 0) continue;
         const int lm = 31 - __clz(p), m = 1 << lm;
@@ -127,27 +127,27 @@ template <int LGC, int S> EPHDC_D int tail_twiddle_index(int s, int g) {
 // WL: 0 = a CTA barrier after every pass; 1 = __syncwarp between warp-local head
 // passes (default: measured fastest, profiles/r01/ab_sync.txt); 2 = also before the
 // tail (windowed pair mapping -- fewer barriers, but slower model-load pattern).
-template <int LGC, int WL = 1, class Load, class H1, class H2>
+template <int LGC, int WL = 1, int E = kE, class Load, class H1, class H2>
 EPHDC_D void fwd_ntt_head(double *buf, const Load &load, const double2 *tw, double nq, const H1 &after_first,
                           const H2 &before_last) {
     static_assert(LGC >= 5, "at least one radix-16 pass before the final stage");
-    fwd_passes<LGC, LGC, true, WL>(buf, load, tw, nq, after_first, before_last);
+    fwd_passes<LGC, LGC, true, WL, E>(buf, load, tw, nq, after_first, before_last);
 }
 
 // Pair index of the last stage.  WINDOWED: thread (warp w, lane l) owns the pairs
 // (2p, 2p+1), p = 256w + l + 32u (u < 8), inside its own warp's window [512w, 512w+512)
 // (so a warp-local last head pass needs no CTA barrier); natural: p = tid + u*NT.
 // Either way the lanes of a warp own consecutive 16-byte pairs (coalesced accesses).
-template <int LGC, bool WINDOWED> EPHDC_D int tail_pair(int u) {
-    if constexpr (WINDOWED) return (threadIdx.x >> 5) * 256 + (threadIdx.x & 31) + 32 * u;
-    else return threadIdx.x + u * ((1 << LGC) / kE);
+template <int LGC, bool WINDOWED, int E = kE> EPHDC_D int tail_pair(int u) {
+    if constexpr (WINDOWED) return (threadIdx.x >> 5) * (E * 16) + (threadIdx.x & 31) + 32 * u;
+    else return threadIdx.x + u * ((1 << LGC) / E);
 }
 
 // Last stage (half-size 1) for the coefficient pair p = tail_pair(u) with its twiddle
 // (w, w/q).  Output order: the CTA's local bit-reversed evaluation order.
-template <int LGC, bool WINDOWED>
+template <int LGC, bool WINDOWED, int E = kE>
 EPHDC_D void fwd_ntt_tail(const double *buf, int u, double w, double wq, double nq, double &x0, double &x1) {
-    const int p = tail_pair<LGC, WINDOWED>(u);
+    const int p = tail_pair<LGC, WINDOWED, E>(u);
     const int a = pad(2 * p);   // 2p is even: 2p + 1 stays in the same 16-word row
     x0 = buf[a];
     x1 = buf[a + 1];
