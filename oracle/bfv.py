@@ -13,6 +13,7 @@ slots = NTT_t(m) (CS3; #20), done with Python big integers.
 from __future__ import annotations
 
 import ctypes
+import math
 from decimal import Decimal, getcontext
 from typing import List, Optional, Tuple
 
@@ -225,7 +226,7 @@ class OracleBFV:
             if r > Q // 2:
                 r -= Q
             worst = max(worst, abs(r))
-        return float(np.log2(worst)) if worst else 0.0
+        return math.log2(worst) if worst else 0.0      # worst can exceed 2^64 (Python int)
 
     def decode_scores(self, cts: np.ndarray, nq: int) -> Tuple[np.ndarray, np.ndarray]:
         """cts [nb][2][L][N] -> centered scores [nq, k] int64 and argmax labels [nq]."""
