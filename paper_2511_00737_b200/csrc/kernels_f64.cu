@@ -101,13 +101,16 @@ __global__ void __launch_bounds__(mac_threads<LGC, E>(), mac_min_blocks<LGC, E>(
     u32 *mst = reinterpret_cast<u32 *>(smem_raw + sizeof(double2) * (NC / 2) +
                                        sizeof(double) * padded_len(NC));               // [N]
     const int tid = threadIdx.x, warp = tid >> 5;
+    // block order: batch fastest, then slice, prime, chunk, group -- the CTAs of a wave
+    // cover bg batches x (a few primes and slices) of one chunk, so a model tile is
+    // read by bg concurrent CTAs and a plaintext row by the slices/primes of the wave
     u32 x = blockIdx.x;
+    const u32 bl = x % a.bg;
+    x /= a.bg;
     const u32 s = x % S;
     x /= S;
     const u32 j = x % a.L;
     x /= a.L;
-    const u32 bl = x % a.bg;
-    x /= a.bg;
     const u32 chunk = x % a.chunks, grp = x / a.chunks;
     const u32 b = grp * a.bg + bl;
     if (b >= a.nb) return;
@@ -628,7 +631,13 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
     f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
     // experiment knobs (profiling only; defaults are the tuned plan)
     a.flags = c->f64_flags_env;
+    if (const char *e = getenv("EPHDC_F64_FLAGS")) a.flags = (u32)strtoul(e, nullptr, 0);
     if (const char *e = getenv("EPHDC_F64_BG")) a.bg = std::max<u32>(1, std::min<u32>(nb, (u32)strtoul(e, nullptr, 0)));
+    if (const char *e = getenv("EPHDC_F64_G")) {  // <= 1024 chunks: the 64-bit fold of f64_grid
+        const u32 gmin = (c->p.D_live + 1023) / 1024;
+        a.G = std::max<u32>(gmin, std::min<u32>(c->p.D_live, (u32)strtoul(e, nullptr, 0)));
+        a.chunks = (c->p.D_live + a.G - 1) / a.G;
+    }
     const uint64_t groups = (nb + a.bg - 1) / a.bg;
     const uint64_t grid = groups * a.chunks * a.bg * c->L * S;
     if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
@@ -717,20 +726,32 @@ bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Pla
     return true;
 }
 
-// Grid of one fused launch over nb batches: batches per group so a group's items of
-// one chunk fill the GPU once (model tiles shared through L2), and the chunk count
-// that minimises waves x dims-per-item.
+// Grid of one fused launch over nb batches (profiles/r01/l2sched: DRAM traffic of the
+// c4 launch 636 -> ~145 GB and -3.5% time against one group of W/(L S) batches with
+// 589-dim chunks).
+//  * Batches per group bg: a wave of W CTAs covers bg batches x W/bg (prime, slice)
+//    pairs of one chunk; each model tile is then fetched ~nb/bg times and each
+//    plaintext row ~L S bg/W times.  With model bytes D L 2N 8 and row bytes nb D N 4
+//    the sum is smallest at bg = sqrt(4W/S), rounded to a whole number of groups.
+//  * Dims per chunk G <= kMaxG, so the CTAs that share a model tile start together
+//    and drift apart by far less than the L2 residency window over a chunk; among
+//    those chunkings the one minimising waves x (G + 1) (one dim of per-CTA setup).
+//  * At most 1024 chunks: the 64-bit atomic fold adds <= chunks values < q < 2^50.
 void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G) {
+    constexpr uint32_t kMaxG = 200;
     const uint32_t S = c->p.log2N >= 14 ? 2 : 1;
     const uint64_t W = 148ull * ntt_mac_f64_occupancy(c->p.log2N);
     const uint64_t LS = (uint64_t)c->L * S;
     const uint32_t D = c->p.D_live;
-    *bg = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nb, W / LS));
+    const double bt = std::sqrt(4.0 * (double)W / (double)S);
+    const uint32_t ngroups = std::max<uint32_t>(1, (uint32_t)std::lround((double)nb / bt));
+    *bg = std::max<uint32_t>(1, (nb + ngroups - 1) / ngroups);
     const uint64_t real = (uint64_t)nb * LS;
-    uint64_t best = ~0ull;
-    uint32_t best_c = 1;
     const uint32_t cmax = std::min<uint32_t>(D, 1024);
-    for (uint32_t ch = 1; ch <= cmax; ++ch) {
+    const uint32_t cmin = std::min<uint32_t>(cmax, (D + kMaxG - 1) / kMaxG);
+    uint64_t best = ~0ull;
+    uint32_t best_c = cmin;
+    for (uint32_t ch = cmin; ch <= cmax; ++ch) {
         const uint64_t g = (D + ch - 1) / ch;
         const uint64_t waves = (real * ch + W - 1) / W;
         const uint64_t cost = waves * (g + 1);

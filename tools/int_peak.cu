@@ -44,6 +44,33 @@ KERNEL(k_mul64lo, uint64_t, 3, asm volatile("mul.lo.u64 %0, %0, %1;" : "+l"(r[c]
 KERNEL(k_dfma, double, 1, asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(r[c]) : "d"(1.0000001)))
 KERNEL(k_dadd, double, 1, asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(r[c]) : "d"(1.0000001)))
 KERNEL(k_dmul, double, 1, asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(r[c]) : "d"(1.0000001)))
+// int32 -> double conversion (I2F.F64): which pipe, what rate
+KERNEL(k_cvt, double, 1, {
+    const int v = __double2loint(r[c]);
+    asm volatile("cvt.rn.f64.s32 %0, %1;" : "=d"(r[c]) : "r"(v));
+})
+// DFMA chains plus as many independent cvt chains: if the conversion has its own pipe
+// this runs at the DFMA-only rate (ops counted = DFMAs only)
+__global__ void k_dfma_cvt(double *out, unsigned long long *clk) {
+    double r[CH], z[CH];
+    for (int c = 0; c < CH; ++c) { r[c] = threadIdx.x * 7 + c; z[c] = c; }
+    unsigned long long c0 = clock64(), g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(r[c]) : "d"(1.0000001));
+            const int v = __double2loint(z[c]);
+            asm volatile("cvt.rn.f64.s32 %0, %1;" : "=d"(z[c]) : "r"(v));
+        }
+    }
+    unsigned long long c1 = clock64(), g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    double s = 0;
+    for (int c = 0; c < CH; ++c) s += r[c] + z[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0 && blockIdx.x == 0) { clk[0] = c1 - c0; clk[1] = g1 - g0; }
+}
 
 // The exact FP64 Cooley-Tukey butterfly of csrc/modf64.cuh (8 FP64 instructions:
 // DMUL, 3 DFMA, 4 DADD) on CH independent (X, Y) pairs: the achievable FP64 rate of
@@ -115,6 +142,8 @@ int main() {
     run<decltype(k_dfma), double>("DFMA(fma.rn.f64)", k_dfma, blocks, threads);
     run<decltype(k_dadd), double>("DADD(add.rn.f64)", k_dadd, blocks, threads);
     run<decltype(k_dmul), double>("DMUL(mul.rn.f64)", k_dmul, blocks, threads);
+    run<decltype(k_cvt), double>("I2F.F64(cvt.rn.f64.s32)", k_cvt, blocks, threads);
+    run<decltype(k_dfma_cvt), double>("DFMA + independent cvt.f64.s32 (DFMA counted)", k_dfma_cvt, blocks, threads);
     // butterfly mix: ITERS/8 iterations x CH butterflies x 8 FP64 instructions = ITERS*CH ops
     run<decltype(k_bfly), double>("FP64 butterfly mix (8 ops/bfly), 8x256 thr/SM", k_bfly, blocks, threads);
     run<decltype(k_bfly), double>("FP64 butterfly mix (8 ops/bfly), 1x512 thr/SM", k_bfly, sms, 512);
