@@ -139,7 +139,7 @@ __global__ void __launch_bounds__((1 << LG) / kE)
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
         const int pos = threadIdx.x + e * NT;
-        const u32 y = csub(mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t), t);
+        const u32 y = csub(mul_shoup_lazy<u32>(buf[sidx<u32>(pos)], a.ninv, a.ninv_p, t), t);
         // encryption inputs stay in [0, t) (Delta * m, reading #4); plaintexts that are
         // multiplied into ciphertexts are stored as their centered lift (reading #3), a
         // signed int32 (|m| < t/2 < 2^29)
@@ -181,11 +181,11 @@ EPHDC_D void inv_pass_perm(u32 *buf, const Load &load, const TwPair<u32> *tw, u3
 #pragma unroll
         for (int kk = 0; kk < R; ++kk) {
             if constexpr (FIRST) x[kk] = load(base + kk * T0);
-            else x[kk] = buf[pad(base + kk * T0)];
+            else x[kk] = buf[sidx<u32>(base + kk * T0)];
         }
         gs_substages<N, T0_LOG, R_LOG, 0>(x, tw, blk, t, two_t);
 #pragma unroll
-        for (int kk = 0; kk < R; ++kk) buf[pad(base + kk * T0)] = x[kk];
+        for (int kk = 0; kk < R; ++kk) buf[sidx<u32>(base + kk * T0)] = x[kk];
     }
     __syncthreads();
 }
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__((1 << LG) / kE, (LG >= 14) ? 1 : (16384 >> LG)
 #pragma unroll
         for (int e = 0; e < kE; ++e) {
             const int pos = tid + e * NT;
-            const u32 y = csub(mul_shoup_lazy<u32>(buf[pad(pos)], a.ninv, a.ninv_p, t), t);
+            const u32 y = csub(mul_shoup_lazy<u32>(buf[sidx<u32>(pos)], a.ninv, a.ninv_p, t), t);
             out[pos] = y <= half_t ? y : (u32)((int)y - (int)t);   // centered lift (reading #3)
         }
         __syncthreads();   // buf is rewritten by the next row's first pass

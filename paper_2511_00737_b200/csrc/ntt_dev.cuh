@@ -4,9 +4,9 @@
 // Each pass runs up to 4 butterfly stages (radix 16) in registers: a thread loads
 // E = 16 elements (E/R groups of R = 2^r elements at stride tl), applies r stages,
 // and writes them back; one __syncthreads() per pass.  Shared memory is padded by
-// one word per 16 (pad(i) = i + i/16) so that every pass pattern, including the
-// 16-consecutive-element groups of the last forward / first inverse pass, is free
-// of bank conflicts.
+// one word per 16 (pad(i) = i + i/16) for 8-byte words and XOR-swizzled for 4-byte
+// words (sidx) so that the pass patterns, including the 16-consecutive-element
+// groups of the last forward / first inverse pass, are free of bank conflicts.
 //
 // Index conventions follow the textbook loops (oracle/oracle_core.c is the
 // independent reference):
@@ -23,6 +23,16 @@ namespace ephdc_ntt {
 
 EPHDC_D int pad(int i) { return i + (i >> 4); }
 constexpr int padded_len(int n) { return n + n / 16; }
+
+// Shared-memory slot of element i of a W buffer.  8-byte words: pad(i) (every pass
+// pattern conflict-free).  4-byte words: the pad layout puts 32 consecutive words in 33
+// banks (a 2-way conflict for the passes whose lanes touch consecutive elements and
+// for the row output); the XOR swizzle i ^ ((i >> 4) & 31) keeps all inverse-pass
+// patterns and the output conflict-free in the same (unpadded) space.
+template <typename W> EPHDC_D int sidx(int i) {
+    if constexpr (sizeof(W) == 4) return i ^ ((i >> 4) & 31);
+    else return pad(i);
+}
 
 // Sub-stages of a forward pass with compile-time trip counts (x[] stays in registers).
 template <typename W, int T0_LOG, int R_LOG, int SUB>
@@ -56,12 +66,12 @@ EPHDC_D void fwd_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ tw
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
-            else x[k] = buf[pad(base + k * TL)];
+            else x[k] = buf[sidx<W>(base + k * TL)];
         }
         const u32 idx0 = (tw_num >> (T0_LOG + 1)) + (u32)blk;
         ct_substages<W, T0_LOG, R_LOG, 0>(x, tw, idx0, q, two_q);
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[pad(base + k * TL)] = x[k];
+        for (int k = 0; k < R; ++k) buf[sidx<W>(base + k * TL)] = x[k];
     }
     __syncthreads();
 }
@@ -76,7 +86,7 @@ EPHDC_D void fwd_passes(W *buf, const Load &load, const TwPair<W> *__restrict__ 
 }
 
 // Forward NTT of NC = 2^LG values produced by load(local_index) (in [0, 4q));
-// result (lazy, [0, 4q)) in buf[pad(i)], bit-reversed evaluation order.
+// result (lazy, [0, 4q)) in buf[sidx<W>(i)], bit-reversed evaluation order.
 template <typename W, int LG, int E, class Load>
 EPHDC_D void fwd_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ tw, u32 tw_num, W q) {
     fwd_passes<W, LG, E, LG, true>(buf, load, tw, tw_num, q, (W)(2 * q));
@@ -114,11 +124,11 @@ EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ it
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             if constexpr (FROM_LOAD) x[k] = load(base + k * T0);
-            else x[k] = buf[pad(base + k * T0)];
+            else x[k] = buf[sidx<W>(base + k * T0)];
         }
         gs_substages<W, LG, T0_LOG, R_LOG, 0>(x, itw, tw_num, blk, q, two_q);
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
+        for (int k = 0; k < R; ++k) buf[sidx<W>(base + k * T0)] = x[k];
     }
     __syncthreads();
 }
@@ -133,7 +143,7 @@ EPHDC_D void inv_passes(W *buf, const Load &load, const TwPair<W> *__restrict__ 
 }
 
 // Inverse NTT (without the final N^-1) of values from load(i) in [0, 2q);
-// result (lazy, [0, 2q)) in buf[pad(i)], natural coefficient order.  As for the
+// result (lazy, [0, 2q)) in buf[sidx<W>(i)], natural coefficient order.  As for the
 // forward transform, tw_num = N + s*NC makes a CTA that owns slice s of a larger
 // transform (the remaining global stages done by the caller) index global blocks.
 template <typename W, int LG, int E, class Load>
