@@ -34,7 +34,7 @@ struct F64MacArgs {
     u32 nb, bg;              // batches in the launch, batches per group (grid order)
     u32 chunks, G;           // dim chunks per batch, dims per chunk
     u32 red_every;           // accumulator reduction interval (dims)
-    u32 flags;               // experiment knobs (EPHDC_F64_FLAGS): bit 0 = no L2 prefetch
+    u32 flags;               // bit 0 = no explicit L2 prefetch of the model slice (launch plan)
 };
 
 // FP64 path plan: chosen at context creation when every q_j < 2^50 and the value

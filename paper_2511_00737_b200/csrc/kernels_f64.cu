@@ -618,20 +618,35 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
                                   cudaStream_t st) {
     // pad shared memory so that no more CTAs share an SM than its TMEM holds
     const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
-    // experiment knob EPHDC_F64_FLAGS bits 1-2: synchronisation variant (fwd_ntt_head WL)
-    const u32 mode = (c->f64_flags_env >> 1) & 3u;
-    // experiment knob bit 3: 32 elements per thread (LGC = 13 only)
-    const bool e32 = LGC == 13 && (c->f64_flags_env & 8u) != 0;
+    // Plan (profiles/r01/ab_wl2.txt): at NC = 2^13 the windowed tail (WL = 2: the last
+    // head pass ends with __syncwarp, 2 CTA barriers per dim) without the explicit L2
+    // prefetch of the model slice is fastest (c4 -5.5%, c3 -1.6%); smaller transforms
+    // keep WL = 1 with the prefetch (c2: WL = 2 is 20% slower).
+    // EPHDC_F64_FLAGS (profiling knob, read per launch) overrides: bits 1-2 = 1/2/3 force
+    // WL = 0/2/1; bit 0 forces the prefetch off, bit 4 on; bit 3 = 32 elements per
+    // thread (LGC = 13 only, WL = 1).
+    u32 env = c->f64_flags_env;
+    if (const char *ev = getenv("EPHDC_F64_FLAGS")) env = (u32)strtoul(ev, nullptr, 0);
+    u32 wl = LGC >= 13 ? 2u : 1u;
+    bool prefetch = LGC < 13;
+    switch ((env >> 1) & 3u) {
+        case 1: wl = 0; break;
+        case 2: wl = 2; break;
+        case 3: wl = 1; break;
+        default: break;
+    }
+    if (env & 1u) prefetch = false;
+    if (env & 16u) prefetch = true;
+    const bool e32 = LGC == 13 && (env & 8u) != 0;
     auto kern = e32 ? k_ntt_mac_f64<LGC, S, 1, 32>
-                    : mode == 1 ? k_ntt_mac_f64<LGC, S, 0, kE> : mode == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;
+                    : wl == 0 ? k_ntt_mac_f64<LGC, S, 0, kE> : wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
     F64MacArgs a = f64_args(c);
     a.nb = nb;
     f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
+    a.flags = prefetch ? 0u : 1u;  // bit 0: no explicit L2 prefetch of the model slice
     // experiment knobs (profiling only; defaults are the tuned plan)
-    a.flags = c->f64_flags_env;
-    if (const char *e = getenv("EPHDC_F64_FLAGS")) a.flags = (u32)strtoul(e, nullptr, 0);
     if (const char *e = getenv("EPHDC_F64_BG")) a.bg = std::max<u32>(1, std::min<u32>(nb, (u32)strtoul(e, nullptr, 0)));
     if (const char *e = getenv("EPHDC_F64_G")) {  // <= 1024 chunks: the 64-bit fold of f64_grid
         const u32 gmin = (c->p.D_live + 1023) / 1024;

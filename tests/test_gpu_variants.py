@@ -1,0 +1,75 @@
+"""Launch-plan variants of the fused FP64 kernel give bit-identical ciphertexts (-m gpu).
+
+The default plan (f64_grid + the WL / prefetch choice in mac_f64_launch) is checked
+against the oracle by test_gpu_fullsize / test_gpu_parity; every other variant the
+EPHDC_F64_* profiling knobs select must produce exactly the same scores ciphertexts:
+the synchronisation variants WL = 0/1/2, 32 elements per thread, the explicit L2
+prefetch on/off, and other grid plans (batches per group, dims per chunk -- i.e. other
+orders of the 64-bit atomic folds, which integer addition makes order independent).
+Each variant's output also decrypts to the brute-force integer scores.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import ephdc_inputs as inp
+from oracle import hdc, pipeline as opipe
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2511_00737_b200 as eph  # noqa: E402
+from paper_2511_00737_b200 import pipeline as ppipe  # noqa: E402
+
+KNOBS = ("EPHDC_F64_FLAGS", "EPHDC_F64_BG", "EPHDC_F64_G")
+VARIANTS = [
+    {"EPHDC_F64_FLAGS": "2"},            # WL = 0: a CTA barrier after every pass
+    {"EPHDC_F64_FLAGS": "6"},            # WL = 1
+    {"EPHDC_F64_FLAGS": "4"},            # WL = 2
+    {"EPHDC_F64_FLAGS": "16"},           # explicit L2 prefetch on
+    {"EPHDC_F64_FLAGS": "1"},            # explicit L2 prefetch off
+    {"EPHDC_F64_FLAGS": "8"},            # 32 elements per thread (NC = 2^13 only)
+    {"EPHDC_F64_BG": "1", "EPHDC_F64_G": "37"},
+    {"EPHDC_F64_BG": "2", "EPHDC_F64_G": "1000"},
+]
+
+
+def _run(ps, ws, H, nq, env):
+    saved = {k: os.environ.pop(k, None) for k in KNOBS}
+    try:
+        os.environ.update(env)
+        out = eph.infer_batch(ps.ctx, ps.model, ws, H, nq)
+        torch.cuda.synchronize()
+        return out.cpu().numpy().view(np.uint64).copy()
+    finally:
+        for k in KNOBS:
+            os.environ.pop(k, None)
+            if saved[k] is not None:
+                os.environ[k] = saved[k]
+
+
+@pytest.mark.parametrize("name,extra", [("c3", 77), ("c4", 123)])
+def test_plan_variants_bit_identical(name, extra):
+    cfg = inp.CONFIGS[name]
+    Xtr, ytr, Xq, _ = inp.gen_features(cfg)
+    P = inp.gen_projection(cfg)
+    ps = ppipe.build(cfg, P, Xtr, ytr)
+    assert ps.ctx.arith == "f64"
+    nq = 2 * ps.ctx.B + extra                      # 3 batches, the last ragged
+    Xs = np.ascontiguousarray(Xq[:nq])
+    X = torch.from_numpy(Xs.view(np.int8)).cuda()
+    H = eph.encode_queries(ps.ctx, X, ps.P_dev)
+    ws = eph.Workspace(ps.ctx, nq)
+    ref = _run(ps, ws, H, nq, {})
+    om = opipe.build_model(cfg, P, Xtr, ytr)
+    H_or = opipe.encode_queries(om, P, Xs)
+    Sref = hdc.scores(H_or, om.class_hv)
+    S, _ = eph.decrypt_scores(ps.ctx, ps.sk, ref, nq)
+    assert np.array_equal(S, Sref)
+    for env in VARIANTS:
+        got = _run(ps, ws, H, nq, env)
+        assert np.array_equal(got, ref), env
