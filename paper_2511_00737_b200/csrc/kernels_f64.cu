@@ -624,7 +624,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
     // keep WL = 1 with the prefetch (c2: WL = 2 is 20% slower).
     // EPHDC_F64_FLAGS (profiling knob, read per launch) overrides: bits 1-2 = 1/2/3 force
     // WL = 0/2/1; bit 0 forces the prefetch off, bit 4 on; bit 3 = 32 elements per
-    // thread (LGC = 13 only, WL = 1).
+    // thread (LGC = 13 only; WL = 2 or 1).
     u32 env = c->f64_flags_env;
     if (const char *ev = getenv("EPHDC_F64_FLAGS")) env = (u32)strtoul(ev, nullptr, 0);
     u32 wl = LGC >= 13 ? 2u : 1u;
@@ -638,7 +638,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
     if (env & 1u) prefetch = false;
     if (env & 16u) prefetch = true;
     const bool e32 = LGC == 13 && (env & 8u) != 0;
-    auto kern = e32 ? k_ntt_mac_f64<LGC, S, 1, 32>
+    auto kern = e32 ? (wl == 2 ? k_ntt_mac_f64<LGC, S, 2, 32> : k_ntt_mac_f64<LGC, S, 1, 32>)
                     : wl == 0 ? k_ntt_mac_f64<LGC, S, 0, kE> : wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;

@@ -134,13 +134,17 @@ EPHDC_D void fwd_ntt_head(double *buf, const Load &load, const double2 *tw, doub
     fwd_passes<LGC, LGC, true, WL, E>(buf, load, tw, nq, after_first, before_last);
 }
 
-// Pair index of the last stage.  WINDOWED: thread (warp w, lane l) owns the pairs
-// (2p, 2p+1), p = 256w + l + 32u (u < 8), inside its own warp's window [512w, 512w+512)
-// (so a warp-local last head pass needs no CTA barrier); natural: p = tid + u*NT.
+// Pair index of the last stage.  WINDOWED: thread (warp w, lane l) owns, for each of its
+// E/16 radix-16 groups v = u/8 (thread group g = tid + v*NT in the head passes), the
+// pairs p = v*8*NT + 256w + l + 32(u%8): exactly the 512-element window that warp w
+// touched with group v in the warp-local head passes ([512w, 512w+512) shifted by
+// v*16*NT), so the last head pass needs no CTA barrier; natural: p = tid + u*NT.
 // Either way the lanes of a warp own consecutive 16-byte pairs (coalesced accesses).
 template <int LGC, bool WINDOWED, int E = kE> EPHDC_D int tail_pair(int u) {
-    if constexpr (WINDOWED) return (threadIdx.x >> 5) * (E * 16) + (threadIdx.x & 31) + 32 * u;
-    else return threadIdx.x + u * ((1 << LGC) / E);
+    constexpr int NT = (1 << LGC) / E;
+    if constexpr (WINDOWED)
+        return (u >> 3) * (8 * NT) + (threadIdx.x >> 5) * 256 + (threadIdx.x & 31) + 32 * (u & 7);
+    else return threadIdx.x + u * NT;
 }
 
 // Last stage (half-size 1) for the coefficient pair p = tail_pair(u) with its twiddle

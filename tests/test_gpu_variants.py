@@ -32,7 +32,9 @@ VARIANTS = [
     {"EPHDC_F64_FLAGS": "4"},            # WL = 2
     {"EPHDC_F64_FLAGS": "16"},           # explicit L2 prefetch on
     {"EPHDC_F64_FLAGS": "1"},            # explicit L2 prefetch off
-    {"EPHDC_F64_FLAGS": "8"},            # 32 elements per thread (NC = 2^13 only)
+    {"EPHDC_F64_FLAGS": "8"},            # 32 elements per thread (NC = 2^13 only), planned WL
+    {"EPHDC_F64_FLAGS": "14"},           # 32 elements per thread, WL = 1
+    {"EPHDC_F64_FLAGS": "12"},           # 32 elements per thread, WL = 2
     {"EPHDC_F64_BG": "1", "EPHDC_F64_G": "37"},
     {"EPHDC_F64_BG": "2", "EPHDC_F64_G": "1000"},
 ]
