@@ -741,26 +741,24 @@ bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Pla
     return true;
 }
 
-// Grid of one fused launch over nb batches (profiles/r01/l2sched: DRAM traffic of the
-// c4 launch 636 -> ~145 GB and -3.5% time against one group of W/(L S) batches with
-// 589-dim chunks).
-//  * Batches per group bg: a wave of W CTAs covers bg batches x W/bg (prime, slice)
-//    pairs of one chunk; each model tile is then fetched ~nb/bg times and each
-//    plaintext row ~L S bg/W times.  With model bytes D L 2N 8 and row bytes nb D N 4
-//    the sum is smallest at bg = sqrt(4W/S), rounded to a whole number of groups.
-//  * Dims per chunk G <= kMaxG, so the CTAs that share a model tile start together
-//    and drift apart by far less than the L2 residency window over a chunk; among
-//    those chunkings the one minimising waves x (G + 1) (one dim of per-CTA setup).
+// Grid of one fused launch over nb batches (profiles/r01/l2sched; ab_grid.txt).
+//  * Block order batch-fastest, all batches in one group (bg = nb, at most one wave):
+//    a wave covers the nb batches x W/nb (prime, slice) pairs of one dim chunk, so each
+//    model tile is fetched about once per chunk by nb concurrent CTAs.  Measured at c4
+//    (one launch): 115-122 GB of DRAM reads with bg = 29, 181 GB with 15, 636 GB with
+//    the earlier prime/slice-fastest order (bg = 8, 589-dim chunks), ~10x the
+//    algorithmic 62 GB.
+//  * Dims per chunk G <= kMaxG, so the CTAs that share a tile start together and stay
+//    within the L2 residency window over a chunk; among those chunkings the one
+//    minimising waves x (G + 2) (two dims' worth of per-CTA setup and fold).
 //  * At most 1024 chunks: the 64-bit atomic fold adds <= chunks values < q < 2^50.
 void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G) {
-    constexpr uint32_t kMaxG = 200;
+    constexpr uint32_t kMaxG = 320;
     const uint32_t S = c->p.log2N >= 14 ? 2 : 1;
     const uint64_t W = 148ull * ntt_mac_f64_occupancy(c->p.log2N);
     const uint64_t LS = (uint64_t)c->L * S;
     const uint32_t D = c->p.D_live;
-    const double bt = std::sqrt(4.0 * (double)W / (double)S);
-    const uint32_t ngroups = std::max<uint32_t>(1, (uint32_t)std::lround((double)nb / bt));
-    *bg = std::max<uint32_t>(1, (nb + ngroups - 1) / ngroups);
+    *bg = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nb, W));
     const uint64_t real = (uint64_t)nb * LS;
     const uint32_t cmax = std::min<uint32_t>(D, 1024);
     const uint32_t cmin = std::min<uint32_t>(cmax, (D + kMaxG - 1) / kMaxG);
@@ -769,7 +767,7 @@ void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, u
     for (uint32_t ch = cmin; ch <= cmax; ++ch) {
         const uint64_t g = (D + ch - 1) / ch;
         const uint64_t waves = (real * ch + W - 1) / W;
-        const uint64_t cost = waves * (g + 1);
+        const uint64_t cost = waves * (g + 2);
         if (cost < best) {
             best = cost;
             best_c = ch;
