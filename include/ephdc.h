@@ -290,6 +290,21 @@ ephdc_status ephdc_decrypt_scores(const ephdc_ctx *ctx, const ephdc_sk *sk, cons
 ephdc_status ephdc_decrypt_slots(const ephdc_ctx *ctx, const ephdc_sk *sk, const uint64_t *h_ct,
                                  uint64_t *h_slots);
 
+/* Noise probe (findDmax, Algorithm 1 l.17-24; NEXT #2), on the GPU.
+ * d_ct [nct][2][L][N]: device scores ciphertexts (NTT form, residues < q_j, e.g.
+ * from ephdc_infer_batch).  For each: x = INTT(c0 + c1 s) mod Q, m = round(t x / Q)
+ * mod t, e = x - floor(Q/t) m centered mod Q; h_bits[b] = EXACT bit length of
+ * max_i |e_i| (0 for e = 0).  Decryption of the ciphertext is correct iff that noise
+ * is below Delta/2; then e is the ciphertext noise (x - Delta m_expected).  h_flags[b]
+ * (may be NULL) = 1 if some t x_i / Q lay within 2^-16 of a rounding boundary (the
+ * decryption itself is ambiguous there), else 0.  h_log2[b] (may be NULL) = log2 of
+ * that maximum from its top 128 bits (0 for e = 0).  Needs a device context; the
+ * secret key's NTT form is uploaded per call.  Synchronous on `stream` (host
+ * outputs).  Errors: ENULL, ECONTEXT (sk of another context, host-only context),
+ * ERESOURCE, ECUDA. */
+ephdc_status ephdc_noise_probe(const ephdc_ctx *ctx, const ephdc_sk *sk, const uint64_t *d_ct, uint32_t nct,
+                               uint32_t *h_bits, uint32_t *h_flags, double *h_log2, void *stream);
+
 /* ---------------- standalone kernels (c5 microbench; CS5) ------------------- */
 
 /* Tables for L primes (each = 1 mod 2N, < 2^61) at ring degree N = 2^log2N,

@@ -215,8 +215,8 @@ class OracleBFV:
         m = np.array([((t * xi + Q // 2) // Q) % t for xi in x], dtype=np.uint64)
         return self.slot_decode(m)
 
-    def noise_bits(self, ct: np.ndarray, slots_expected: np.ndarray) -> float:
-        """log2 of the infinity norm of x - Delta*m_expected (centered mod Q)."""
+    def noise_max(self, ct: np.ndarray, slots_expected: np.ndarray) -> int:
+        """Infinity norm of x - Delta*m_expected (centered mod Q), an exact Python int."""
         x = self.decrypt_poly(ct)
         m = self.slot_encode(np.asarray(slots_expected, dtype=np.int64) % self.t).tolist()
         Q, dl = self.Q, self.delta_big
@@ -226,6 +226,11 @@ class OracleBFV:
             if r > Q // 2:
                 r -= Q
             worst = max(worst, abs(r))
+        return worst
+
+    def noise_bits(self, ct: np.ndarray, slots_expected: np.ndarray) -> float:
+        """log2 of the infinity norm of x - Delta*m_expected (centered mod Q)."""
+        worst = self.noise_max(ct, slots_expected)
         return math.log2(worst) if worst else 0.0      # worst can exceed 2^64 (Python int)
 
     def decode_scores(self, cts: np.ndarray, nq: int) -> Tuple[np.ndarray, np.ndarray]:

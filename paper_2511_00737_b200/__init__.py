@@ -340,6 +340,19 @@ def decrypt_slots(ctx: Context, sk: SecretKey, ct: np.ndarray) -> np.ndarray:
     return out
 
 
+def noise_probe(ctx: Context, sk: SecretKey, cts, stream=None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """ephdc_noise_probe: per device scores ciphertext of cts [nct][2][L][N] (torch int64
+    on the GPU) the exact bit length of the decryption noise, the rounding-ambiguity flag
+    and log2 of the noise (findDmax)."""
+    nct = int(cts.shape[0]) if cts.dim() == 4 else 1
+    bits = np.zeros(nct, dtype=np.uint32)
+    flags = np.zeros(nct, dtype=np.uint32)
+    lg = np.zeros(nct, dtype=np.float64)
+    call("ephdc_noise_probe", ctx.handle, sk.handle, _dptr(cts), nct, _np_ptr(bits), _np_ptr(flags), _np_ptr(lg),
+         _stream(stream))
+    return bits, flags, lg
+
+
 # --------------------------------------------------------------------------- standalone (c5)
 class NttPlan:
     def __init__(self, q: Sequence[int], log2N: int, device: int = 0):

@@ -85,6 +85,7 @@ _SIGS = {
     "ephdc_unpack_scores": (c_st, [c_vp, c_vp, c_u32, c_vp]),
     "ephdc_classify_host_packed": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
     "ephdc_decrypt_slots": (c_st, [c_vp, c_vp, c_vp, c_vp]),
+    "ephdc_noise_probe": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
     "ephdc_ntt_plan_create": (c_st, [c_vp, c_u32, c_u32, c_int, c_vp]),
     "ephdc_ntt_plan_free": (None, [c_vp]),
     "ephdc_ntt_fwd": (c_st, [c_vp, c_vp, c_u32, c_vp]),
