@@ -25,6 +25,9 @@ EPHDC_D u32 mulhi(u32 a, u32 b) { return __umulhi(a, b); }
 template <typename W> EPHDC_D W mul_shoup_lazy(W x, W w, W wp, W q) { return x * w - mulhi(x, wp) * q; }
 
 template <typename W> EPHDC_D W csub(W x, W m) { return x >= m ? x - m : x; }
+// u32, x < 2m: x - m wraps above x exactly when x < m, so min() selects -- IADD + VIMNMX
+// instead of ISETP + SEL + IADD
+template <> EPHDC_D u32 csub<u32>(u32 x, u32 m) { return min(x, x - m); }
 
 // Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> X + wY, X - wY in [0, 4q)
 template <typename W>
