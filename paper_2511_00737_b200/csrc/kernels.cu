@@ -136,10 +136,11 @@ __global__ void __launch_bounds__((1 << LG) / kE)
     inv_ntt<u32, LG, kE>(buf, load, a.itw, t);
     u32 *out = M + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * N;
     const u32 half_t = (t - 1) / 2;
+    const int stid = sidx<u32>(threadIdx.x);
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
         const int pos = threadIdx.x + e * NT;
-        const u32 y = csub(mul_shoup_lazy<u32>(buf[sidx<u32>(pos)], a.ninv, a.ninv_p, t), t);
+        const u32 y = csub(mul_shoup_lazy<u32>(buf[sidx_at<u32>(stid, e * NT)], a.ninv, a.ninv_p, t), t);
         // encryption inputs stay in [0, t) (Delta * m, reading #4); plaintexts that are
         // multiplied into ciphertexts are stored as their centered lift (reading #3), a
         // signed int32 (|m| < t/2 < 2^29)
@@ -177,15 +178,16 @@ EPHDC_D void inv_pass_perm(u32 *buf, const Load &load, const TwPair<u32> *tw, u3
         const int g = tid + u * NT;
         const int blk = g >> T0_LOG, off = g & (T0 - 1);
         const int base = blk * (T0 * R) + off;
+        const int sb = sidx<u32>(base);
         u32 x[R];
 #pragma unroll
         for (int kk = 0; kk < R; ++kk) {
             if constexpr (FIRST) x[kk] = load(base + kk * T0);
-            else x[kk] = buf[sidx<u32>(base + kk * T0)];
+            else x[kk] = buf[sidx_at<u32>(sb, kk * T0)];
         }
         gs_substages<N, T0_LOG, R_LOG, 0>(x, tw, blk, t, two_t);
 #pragma unroll
-        for (int kk = 0; kk < R; ++kk) buf[sidx<u32>(base + kk * T0)] = x[kk];
+        for (int kk = 0; kk < R; ++kk) buf[sidx_at<u32>(sb, kk * T0)] = x[kk];
     }
     __syncthreads();
 }
@@ -240,10 +242,11 @@ __global__ void __launch_bounds__((1 << LG) / kE, (LG >= 14) ? 1 : (16384 >> LG)
         };
         inv_passes_perm<LG, 0, true>(buf, load, tw, t, two_t);
         u32 *out = M + (size_t)row * N;
+        const int stid = sidx<u32>(tid);
 #pragma unroll
         for (int e = 0; e < kE; ++e) {
             const int pos = tid + e * NT;
-            const u32 y = csub(mul_shoup_lazy<u32>(buf[sidx<u32>(pos)], a.ninv, a.ninv_p, t), t);
+            const u32 y = csub(mul_shoup_lazy<u32>(buf[sidx_at<u32>(stid, e * NT)], a.ninv, a.ninv_p, t), t);
             out[pos] = y <= half_t ? y : (u32)((int)y - (int)t);   // centered lift (reading #3)
         }
         __syncthreads();   // buf is rewritten by the next row's first pass

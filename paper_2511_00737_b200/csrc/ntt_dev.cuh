@@ -33,6 +33,18 @@ template <typename W> EPHDC_D int sidx(int i) {
     if constexpr (sizeof(W) == 4) return i ^ ((i >> 4) & 31);
     else return pad(i);
 }
+// Slot of element base + c where base and the compile-time offset c share no set bits
+// (a pass group: base = blk * block + off, c = k * stride).  The u32 swizzle is
+// XOR-linear, so sidx(base + c) = sidx(base) ^ sidx(c): one LOP3 with an immediate per
+// element.  sb = sidx<W>(base) for 4-byte words, base for 8-byte words.
+template <typename W> EPHDC_D int sidx_at(int sb, int c) {
+    if constexpr (sizeof(W) == 4) return sb ^ sidx<W>(c);
+    else return pad(sb + c);
+}
+template <typename W> EPHDC_D int sidx_base(int base) {
+    if constexpr (sizeof(W) == 4) return sidx<W>(base);
+    else return base;
+}
 
 // Sub-stages of a forward pass with compile-time trip counts (x[] stays in registers).
 template <typename W, int T0_LOG, int R_LOG, int SUB>
@@ -62,16 +74,17 @@ EPHDC_D void fwd_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ tw
         const int g = tid + u * NT;
         const int blk = g >> TL_LOG, off = g & (TL - 1);
         const int base = (blk << (T0_LOG + 1)) + off;
+        const int sb = sidx_base<W>(base);
         W x[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
-            else x[k] = buf[sidx<W>(base + k * TL)];
+            else x[k] = buf[sidx_at<W>(sb, k * TL)];
         }
         const u32 idx0 = (tw_num >> (T0_LOG + 1)) + (u32)blk;
         ct_substages<W, T0_LOG, R_LOG, 0>(x, tw, idx0, q, two_q);
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[sidx<W>(base + k * TL)] = x[k];
+        for (int k = 0; k < R; ++k) buf[sidx_at<W>(sb, k * TL)] = x[k];
     }
     __syncthreads();
 }
@@ -120,15 +133,16 @@ EPHDC_D void inv_pass(W *buf, const Load &load, const TwPair<W> *__restrict__ it
         const int g = tid + u * NT;
         const int blk = g >> T0_LOG, off = g & (T0 - 1);
         const int base = blk * (T0 * R) + off;
+        const int sb = sidx_base<W>(base);
         W x[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             if constexpr (FROM_LOAD) x[k] = load(base + k * T0);
-            else x[k] = buf[sidx<W>(base + k * T0)];
+            else x[k] = buf[sidx_at<W>(sb, k * T0)];
         }
         gs_substages<W, LG, T0_LOG, R_LOG, 0>(x, itw, tw_num, blk, q, two_q);
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[sidx<W>(base + k * T0)] = x[k];
+        for (int k = 0; k < R; ++k) buf[sidx_at<W>(sb, k * T0)] = x[k];
     }
     __syncthreads();
 }
