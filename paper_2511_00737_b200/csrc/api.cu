@@ -819,7 +819,7 @@ void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
         cudaFree(p->ninv);
         cudaFree(p->tw_f64);
         cudaFree(p->itw_f64);
-        cudaFree(p->ninv_f64);
+        cudaFree(p->post_f64);
     }
     delete p;
 }
@@ -854,33 +854,60 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
         ninv[2 * j] = invmod(N % q[j], q[j]);
         ninv[2 * j + 1] = shoup64(ninv[2 * j], q[j]);
     }
-    plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64);
+    plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
     if (const char *e = getenv("EPHDC_NTT_INT")) {  // profiling knob: force the integer kernels
         if (atoi(e)) p->fwd_f64 = p->inv_f64 = false;
     }
     if (p->fwd_f64 || p->inv_f64) {
-        std::vector<double> f((size_t)L * N * 2), g((size_t)L * N * 2), ni(2 * L);
+        // FP64 tables: forward psi_rev; inverse = Cooley-Tukey DIT on the bit-reversed
+        // input (x[r] = DFT(a psi^j)[brev r]): stage of half-size h uses omega^-(N/2h) jj
+        // for the block position jj < h (entry h + jj), then a_j = N^-1 psi^-j x_j
+        std::vector<double> f((size_t)L * N * 2), g((size_t)L * N * 2), po((size_t)L * N * 2);
         for (uint32_t j = 0; j < L; ++j) {
             const double qd = (double)q[j];
+            const uint64_t psi_inv = invmod(min_primitive_root_2n(q[j], log2N), q[j]);
             for (uint32_t i = 0; i < N; ++i) {
                 const size_t k = (size_t)j * N + i;
                 f[2 * k] = i ? (double)tw[k].w : qd;
                 f[2 * k + 1] = i ? (double)tw[k].w / qd : 1.0 / qd;
-                g[2 * k] = i ? (double)itw[k].w : qd;
-                g[2 * k + 1] = i ? (double)itw[k].w / qd : 1.0 / qd;
             }
-            ni[2 * j] = (double)ninv[2 * j];
-            ni[2 * j + 1] = (double)ninv[2 * j] / qd;
+            g[2 * (size_t)j * N] = qd;
+            g[2 * (size_t)j * N + 1] = 1.0 / qd;
+            if (p->inv_dit) {
+                for (uint32_t h = 1; h < N; h *= 2) {
+                    const uint64_t wh = powmod(psi_inv, N / h, q[j]);   // omega^-(N/2h), omega = psi^2
+                    uint64_t w = 1;
+                    for (uint32_t jj = 0; jj < h; ++jj, w = mulmod(w, wh, q[j])) {
+                        const size_t k = (size_t)j * N + h + jj;
+                        g[2 * k] = (double)w;
+                        g[2 * k + 1] = (double)w / qd;
+                    }
+                }
+                uint64_t c = ninv[2 * j];                                  // N^-1 psi^-i
+                for (uint32_t i = 0; i < N; ++i, c = mulmod(c, psi_inv, q[j])) {
+                    const size_t k = (size_t)j * N + i;
+                    po[2 * k] = (double)c;
+                    po[2 * k + 1] = (double)c / qd;
+                }
+            } else {
+                for (uint32_t i = 1; i < N; ++i) {                       // psi^-1_rev (GS)
+                    const size_t k = (size_t)j * N + i;
+                    g[2 * k] = (double)itw[k].w;
+                    g[2 * k + 1] = (double)itw[k].w / qd;
+                }
+                po[2 * (size_t)j * N] = (double)ninv[2 * j];           // [j][0] = N^-1
+                po[2 * (size_t)j * N + 1] = (double)ninv[2 * j] / qd;
+            }
         }
         if (cudaMalloc(&p->tw_f64, sizeof(double) * f.size()) != cudaSuccess ||
             cudaMalloc(&p->itw_f64, sizeof(double) * g.size()) != cudaSuccess ||
-            cudaMalloc(&p->ninv_f64, sizeof(double) * ni.size()) != cudaSuccess) {
+            cudaMalloc(&p->post_f64, sizeof(double) * po.size()) != cudaSuccess) {
             ephdc_ntt_plan_free(p.release());
             return EPHDC_ERESOURCE;
         }
         if (cudaMemcpy(p->tw_f64, f.data(), sizeof(double) * f.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(p->itw_f64, g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(p->ninv_f64, ni.data(), sizeof(double) * ni.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaMemcpy(p->post_f64, po.data(), sizeof(double) * po.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
             ephdc_ntt_plan_free(p.release());
             return EPHDC_ECUDA;
         }

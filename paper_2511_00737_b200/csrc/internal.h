@@ -117,8 +117,12 @@ struct ephdc_ntt_plan {
     uint64_t *ninv = nullptr;                            // [L][2] (N^-1, Shoup)
     // FP64 path (kernels_f64.cu k_ntt_std_f64) when the bounds allow it
     bool fwd_f64 = false, inv_f64 = false;
-    double2 *tw_f64 = nullptr, *itw_f64 = nullptr;       // [L][N] (w, w/q); entry 0 = (q, 1/q)
-    double2 *ninv_f64 = nullptr;                         // [L] (N^-1, N^-1/q)
+    bool inv_dit = false;   // FP64 inverse form: Cooley-Tukey DIT (true) or Gentleman-Sande
+    // FP64 path: forward psi_rev table and the inverse's table -- GS: psi^-1_rev; DIT:
+    // stage table (entry h + jj = omega^-(N/2h) jj) -- each [L][N] (w, w/q) with entry
+    // 0 = (q, 1/q); the inverse's scaling: GS N^-1 [L], DIT N^-1 psi^-j [L][N] (w, w/q)
+    double2 *tw_f64 = nullptr, *itw_f64 = nullptr;
+    double2 *post_f64 = nullptr;
 };
 
 namespace ephdc {
@@ -176,12 +180,12 @@ cudaError_t launch_reduce_out(const ephdc_ctx *c, uint64_t *d_out, uint32_t nb, 
 int ntt_mac_f64_occupancy(uint32_t log2N);
 struct StdF64Args {
     u32 L;
-    const double2 *tw;     // [L][N] forward or inverse (w, w/q); entry 0 = (q, 1/q)
-    const double2 *ninv;   // [L] (N^-1, N^-1/q)
+    const double2 *tw;     // [L][N] forward (psi_rev) or inverse (DIT stages) (w, w/q); entry 0 = (q, 1/q)
+    const double2 *post;   // inverse scaling: GS [L] N^-1, DIT [L][N] N^-1 psi^-j (w, w/q)
 };
 cudaError_t launch_ntt_batch_f64(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t batch, bool inverse,
                                  cudaStream_t st);
-void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv);
+void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv, bool *inv_dit);
 bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan);
 void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G);
 int ntt_mac_occupancy(uint32_t log2N, uint32_t S);

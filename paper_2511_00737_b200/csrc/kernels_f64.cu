@@ -336,8 +336,11 @@ __global__ void EPHDC_F64_BOUNDS(LGC)
 // cluster barrier after the first pass keeps either CTA from overwriting input its
 // partner still reads.  Inverse: S = 1 (N <= 2^13).
 // =====================================================================================
-template <int LGC, int S, bool INV>
+// DIR: 0 forward, 1 inverse Gentleman-Sande (bound doubles per stage: small primes),
+// 2 inverse Cooley-Tukey DIT (linear bound growth, per-coefficient N^-1 psi^-j)
+template <int LGC, int S, int DIR>
 __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restrict__ polys, u32 batch, StdF64Args a) {
+    constexpr bool INV = DIR != 0;
     constexpr int NC = 1 << LGC, N = NC * S;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *tw = reinterpret_cast<double2 *>(smem_raw);
@@ -349,11 +352,17 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
     const double2 *twg = a.tw + (size_t)j * N;
     const double2 qq = twg[0];
     const double q = qq.x, nq = -q, qinv = qq.y, half_q = 0.5 * q;
-    if constexpr (INV) load_inv_twiddles<LGC>(tw, twg);
-    else load_twiddles<LGC, S>(tw, twg, (int)s, NC);
+    if constexpr (DIR == 2) {
+        for (int p = tid; p < NC; p += NC / kE) tw[p] = twg[p];   // DIT stage table, natural order
+    } else if constexpr (DIR == 1) {
+        load_inv_twiddles<LGC>(tw, twg);
+    } else {
+        load_twiddles<LGC, S>(tw, twg, (int)s, NC);
+    }
     double2 w1 = make_double2(0.0, 0.0);
     if constexpr (S > 1) w1 = twg[1];
-    const double2 ni = INV ? a.ninv[j] : make_double2(0.0, 0.0);
+    const double2 *post = a.post + (size_t)j * N;   // inverse: N^-1 psi^-i (DIT), N^-1 at [0] (GS)
+    const double2 ni = DIR == 1 ? post[0] : make_double2(0.0, 0.0);
     __syncthreads();
     auto centered = [&](u64 v) -> double {   // [0, q) -> (-q/2, q/2]
         const double x = from_u64(v);
@@ -400,12 +409,14 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
             auto load = [&](int pos) -> double {
                 return centered(__ldcs(reinterpret_cast<const unsigned long long *>(p + pos)));
             };
-            inv_ntt_f64<LGC, 0, true>(buf, load, tw, nq);
+            if constexpr (DIR == 2) inv_dit_f64<LGC, 0, true>(buf, load, tw, nq);
+            else inv_ntt_f64<LGC, 0, true>(buf, load, tw, nq);
             constexpr int NT = NC / kE;
 #pragma unroll
             for (int e = 0; e < kE; ++e) {
                 const int pos = tid + e * NT;
-                const double y = reduce(mul_tw(buf[pad(pos)], ni.x, ni.y, nq), qinv, nq);
+                const double2 c = DIR == 2 ? post[pos] : ni;
+                const double y = reduce(mul_tw(buf[pad(pos)], c.x, c.y, nq), qinv, nq);
                 __stcs(reinterpret_cast<unsigned long long *>(p + pos), (unsigned long long)to_canonical_u64(y, q));
             }
         }
@@ -413,16 +424,17 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
     }
 }
 
-template <int LGC, int S, bool INV>
+template <int LGC, int S, int DIR>
 static cudaError_t std_f64_launch(const ephdc_ntt_plan *pl, u64 *polys, u32 batch, cudaStream_t st) {
+    constexpr bool INV = DIR != 0;
     const size_t smem = sizeof(double2) * ((size_t)1 << LGC) + sizeof(double) * (size_t)padded_len(1 << LGC);
-    auto kern = k_ntt_std_f64<LGC, S, INV>;
+    auto kern = k_ntt_std_f64<LGC, S, DIR>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
     StdF64Args a;
     a.L = pl->L;
     a.tw = INV ? pl->itw_f64 : pl->tw_f64;
-    a.ninv = pl->ninv_f64;
+    a.post = pl->post_f64;
     // workers per prime: fill the GPU (CTAs per SM from shared memory), at most batch
     const int per_sm = std::max<int>(1, (int)((228u << 10) / (smem + 1024)));
     const uint64_t ctas = 148ull * per_sm;
@@ -452,47 +464,60 @@ cudaError_t launch_ntt_batch_f64(const ephdc_ntt_plan *pl, uint64_t *d_polys, ui
     if (batch == 0) return cudaSuccess;
     if (!inverse) {
         switch (pl->log2N) {
-            case 10: return std_f64_launch<10, 1, false>(pl, d_polys, batch, st);
-            case 11: return std_f64_launch<11, 1, false>(pl, d_polys, batch, st);
-            case 12: return std_f64_launch<12, 1, false>(pl, d_polys, batch, st);
-            case 13: return std_f64_launch<13, 1, false>(pl, d_polys, batch, st);
-            case 14: return std_f64_launch<13, 2, false>(pl, d_polys, batch, st);
+            case 10: return std_f64_launch<10, 1, 0>(pl, d_polys, batch, st);
+            case 11: return std_f64_launch<11, 1, 0>(pl, d_polys, batch, st);
+            case 12: return std_f64_launch<12, 1, 0>(pl, d_polys, batch, st);
+            case 13: return std_f64_launch<13, 1, 0>(pl, d_polys, batch, st);
+            case 14: return std_f64_launch<13, 2, 0>(pl, d_polys, batch, st);
+        }
+    } else if (pl->inv_dit) {
+        switch (pl->log2N) {
+            case 10: return std_f64_launch<10, 1, 2>(pl, d_polys, batch, st);
+            case 11: return std_f64_launch<11, 1, 2>(pl, d_polys, batch, st);
+            case 12: return std_f64_launch<12, 1, 2>(pl, d_polys, batch, st);
+            case 13: return std_f64_launch<13, 1, 2>(pl, d_polys, batch, st);
         }
     } else {
         switch (pl->log2N) {
-            case 10: return std_f64_launch<10, 1, true>(pl, d_polys, batch, st);
-            case 11: return std_f64_launch<11, 1, true>(pl, d_polys, batch, st);
-            case 12: return std_f64_launch<12, 1, true>(pl, d_polys, batch, st);
-            case 13: return std_f64_launch<13, 1, true>(pl, d_polys, batch, st);
+            case 10: return std_f64_launch<10, 1, 1>(pl, d_polys, batch, st);
+            case 11: return std_f64_launch<11, 1, 1>(pl, d_polys, batch, st);
+            case 12: return std_f64_launch<12, 1, 1>(pl, d_polys, batch, st);
+            case 13: return std_f64_launch<13, 1, 1>(pl, d_polys, batch, st);
         }
     }
     return cudaErrorNotSupported;
 }
 
 // Bounds of the standalone FP64 transforms: canonical inputs are
-// centered (|x| <= q/2); forward CT stages add <= (1/2 + B 2^-54) q each, inverse GS
-// stages double the bound; every mul_tw input must stay below 2^51.
-void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv) {
+// centered (|x| <= q/2); forward CT stages and the inverse's CT DIT stages add
+// <= (1/2 + B 2^-54) q each, inverse GS stages double the bound; every mul_tw input --
+// for the inverse also the final scaling product -- must stay below 2^51.  The
+// inverse uses GS where its bound allows (small primes: no per-coefficient scaling
+// table to stream, measured faster), else DIT (profiles/r01/c5/ab_inv_dit.txt).
+void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv, bool *inv_dit) {
     const double L51 = 0.98 * 2251799813685248.0, e54 = 1.0 / 18014398509481984.0;
     *fwd = log2N >= 10 && log2N <= 14;
-    *inv = log2N >= 10 && log2N <= 13;
+    bool gs = log2N >= 10 && log2N <= 13, dit = gs;
     for (uint64_t qj : q) {
         if (qj >= (1ull << 50)) {
-            *fwd = *inv = false;
+            *fwd = *inv = *inv_dit = false;
             return;
         }
         const double Q = (double)qj;
         double B = Q / 2 + 1;
         for (uint32_t st = 0; st < log2N; ++st) {
-            if (B >= L51) *fwd = false;
+            if (B >= L51) *fwd = dit = false;
             B += (0.5 + B * e54) * Q + 2.0;
         }
+        if (B >= L51) dit = false;
         double Bi = Q / 2 + 1;
         for (uint32_t st = 0; st < log2N; ++st) {
-            if (2 * Bi >= L51) *inv = false;
+            if (2 * Bi >= L51) gs = false;
             Bi *= 2;
         }
     }
+    *inv = gs || dit;
+    *inv_dit = !gs && dit;
 }
 
 // model residues u64 -> exact doubles, in place (setup, once per model)

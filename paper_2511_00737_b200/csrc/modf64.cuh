@@ -63,6 +63,9 @@ EPHDC_D void ct_bfly(double &X, double &Y, double w, double wq, double nq) {
     Y = __dsub_rn(x, t);
 }
 
+
+// Exact conversions without the I2F/F2I conversion unit: an integer v < 2^52 placed in
+// the mantissa of 2^52 (bit pattern 0x4330... | v) is the double 2^52 + v.
 // Gentleman-Sande butterfly (X, Y) -> (X + Y, (X - Y) w).
 EPHDC_D void gs_bfly(double &X, double &Y, double w, double wq, double nq) {
     const double x = X, y = Y;
@@ -70,8 +73,6 @@ EPHDC_D void gs_bfly(double &X, double &Y, double w, double wq, double nq) {
     Y = mul_tw(__dsub_rn(x, y), w, wq, nq);
 }
 
-// Exact conversions without the I2F/F2I conversion unit: an integer v < 2^52 placed in
-// the mantissa of 2^52 (bit pattern 0x4330... | v) is the double 2^52 + v.
 EPHDC_D double from_u64(uint64_t v) {  // v < 2^52
     return __dsub_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), kTwo52);
 }

@@ -225,4 +225,58 @@ EPHDC_D void load_inv_twiddles(double2 *tw_s, const double2 *__restrict__ twg) {
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Inverse as Cooley-Tukey DIT (standalone c5 transform): the forward output x (bit-
+// reversed) is DFT(a psi^j) permuted, so DIT stages with half-sizes 1, 2, ..., NC/2 and
+// twiddles omega^-(NC/2h) jj (jj = position in the block of 2h) produce
+// IDFT(DFT(a psi^j)) = NC a_j psi^j in natural order; the caller multiplies by
+// NC^-1 psi^-j.  CT butterflies grow the bound by <= (1/2 + B 2^-54) q per stage, as in
+// the forward transform (the GS form doubles it per stage).  Twiddles: the stage table
+// tw[h + jj] (natural order; a warp's lanes read consecutive or identical entries).
+// ---------------------------------------------------------------------------------
+template <int T0_LOG, int R_LOG, int SUB>
+EPHDC_D void dit_substages_f64(double (&x)[1 << R_LOG], const double2 *tw, int off, double nq) {
+    if constexpr (SUB < R_LOG) {
+        constexpr int R = 1 << R_LOG, hs = 1 << SUB, T0 = 1 << T0_LOG, h = hs * T0;
+#pragma unroll
+        for (int kk = 0; kk < hs; ++kk) {
+            const double2 w = tw[h + off + kk * T0];
+#pragma unroll
+            for (int v = 0; v < R / (2 * hs); ++v) ct_bfly(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w.x, w.y, nq);
+        }
+        dit_substages_f64<T0_LOG, R_LOG, SUB + 1>(x, tw, off, nq);
+    }
+}
+
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+EPHDC_D void dit_pass_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+    constexpr int NC = 1 << LGC, NT = NC / kE, R = 1 << R_LOG, T0 = 1 << T0_LOG;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kE / R; ++u) {
+        const int g = tid + u * NT;
+        const int blk = g >> T0_LOG, off = g & (T0 - 1);
+        const int base = blk * (T0 * R) + off;
+        double x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            if constexpr (FROM_LOAD) x[k] = load(base + k * T0);
+            else x[k] = buf[pad(base + k * T0)];
+        }
+        dit_substages_f64<T0_LOG, R_LOG, 0>(x, tw, off, nq);
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
+    }
+    __syncthreads();
+}
+
+template <int LGC, int DONE, bool FIRST, class Load>
+EPHDC_D void inv_dit_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+    if constexpr (DONE < LGC) {
+        constexpr int R_LOG = (LGC - DONE) >= 4 ? 4 : (LGC - DONE);
+        dit_pass_f64<LGC, DONE, R_LOG, FIRST>(buf, load, tw, nq);
+        inv_dit_f64<LGC, DONE + R_LOG, false>(buf, load, tw, nq);
+    }
+}
+
 }  // namespace ephdc_f64
