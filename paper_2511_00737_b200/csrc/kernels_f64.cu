@@ -406,19 +406,20 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
                 __stcs(reinterpret_cast<ulonglong2 *>(o + 2 * g), v);
             }
         } else {
+            // the first inverse pass reads 16 consecutive residues per thread (lanes 128 B
+            // apart): L1-allocating loads so each 32-byte sector is fetched once
             auto load = [&](int pos) -> double {
-                return centered(__ldcs(reinterpret_cast<const unsigned long long *>(p + pos)));
+                return centered(__ldg(reinterpret_cast<const unsigned long long *>(p + pos)));
             };
-            if constexpr (DIR == 2) inv_dit_f64<LGC, 0, true>(buf, load, tw, nq);
-            else inv_ntt_f64<LGC, 0, true>(buf, load, tw, nq);
-            constexpr int NT = NC / kE;
-#pragma unroll
-            for (int e = 0; e < kE; ++e) {
-                const int pos = tid + e * NT;
+            // the last pass scales and stores straight to global memory (its lanes hold
+            // consecutive positions: coalesced)
+            auto sink = [&](int pos, double x) {
                 const double2 c = DIR == 2 ? post[pos] : ni;
-                const double y = reduce(mul_tw(buf[pad(pos)], c.x, c.y, nq), qinv, nq);
+                const double y = reduce(mul_tw(x, c.x, c.y, nq), qinv, nq);
                 __stcs(reinterpret_cast<unsigned long long *>(p + pos), (unsigned long long)to_canonical_u64(y, q));
-            }
+            };
+            if constexpr (DIR == 2) inv_dit_f64<LGC, 0, true>(buf, load, tw, nq, sink);
+            else inv_ntt_f64<LGC, 0, true>(buf, load, tw, nq, sink);
         }
         __syncthreads();   // buf is rewritten by the next polynomial
     }

@@ -178,8 +178,21 @@ EPHDC_D void gs_substages_f64(double (&x)[1 << R_LOG], const double2 *tw, int bl
     }
 }
 
-template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
-EPHDC_D void inv_pass_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+// SINK: the last pass hands each output (natural position, value) to sink() -- the
+// caller's scaling + global store -- instead of writing shared memory (no barrier).
+// Inverse passes run with increasing half-sizes; a radix-16 pass with T0 <= 32 keeps
+// each warp in the window [512w, 512w + 512) (one group per thread, blocks of 16 T0
+// <= 512 elements), so between two such passes a __syncwarp suffices.
+template <int LGC, int T0_LOG, int R_LOG> constexpr bool inv_warp_local() {
+    return R_LOG == 4 && T0_LOG <= 5 && ((1 << LGC) / kE) % 32 == 0;
+}
+template <int LGC, int DONE> constexpr bool inv_next_warp_local() {
+    constexpr int NEXT = DONE + ((LGC - DONE) >= 4 ? 4 : (LGC - DONE));
+    if constexpr (NEXT >= LGC) return false;
+    else return inv_warp_local<LGC, NEXT, ((LGC - NEXT) >= 4 ? 4 : (LGC - NEXT))>();
+}
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, bool SINK, class Load, class Sink>
+EPHDC_D void inv_pass_f64(double *buf, const Load &load, const double2 *tw, double nq, const Sink &sink) {
     constexpr int NC = 1 << LGC, NT = NC / kE, R = 1 << R_LOG, T0 = 1 << T0_LOG;
     const int tid = threadIdx.x;
 #pragma unroll
@@ -195,17 +208,23 @@ EPHDC_D void inv_pass_f64(double *buf, const Load &load, const double2 *tw, doub
         }
         gs_substages_f64<NC, T0_LOG, R_LOG, 0>(x, tw, blk, nq);
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
+        for (int k = 0; k < R; ++k) {
+            if constexpr (SINK) sink(base + k * T0, x[k]);
+            else buf[pad(base + k * T0)] = x[k];
+        }
     }
-    __syncthreads();
+    if constexpr (!SINK) {
+        if constexpr (inv_warp_local<LGC, T0_LOG, R_LOG>() && inv_next_warp_local<LGC, T0_LOG>()) __syncwarp();
+        else __syncthreads();
+    }
 }
 
-template <int LGC, int DONE, bool FIRST, class Load>
-EPHDC_D void inv_ntt_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+template <int LGC, int DONE, bool FIRST, class Load, class Sink>
+EPHDC_D void inv_ntt_f64(double *buf, const Load &load, const double2 *tw, double nq, const Sink &sink) {
     if constexpr (DONE < LGC) {
         constexpr int R_LOG = (LGC - DONE) >= 4 ? 4 : (LGC - DONE);
-        inv_pass_f64<LGC, DONE, R_LOG, FIRST>(buf, load, tw, nq);
-        inv_ntt_f64<LGC, DONE + R_LOG, false>(buf, load, tw, nq);
+        inv_pass_f64<LGC, DONE, R_LOG, FIRST, DONE + R_LOG == LGC>(buf, load, tw, nq, sink);
+        inv_ntt_f64<LGC, DONE + R_LOG, false>(buf, load, tw, nq, sink);
     }
 }
 
@@ -248,8 +267,8 @@ EPHDC_D void dit_substages_f64(double (&x)[1 << R_LOG], const double2 *tw, int o
     }
 }
 
-template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
-EPHDC_D void dit_pass_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, bool SINK, class Load, class Sink>
+EPHDC_D void dit_pass_f64(double *buf, const Load &load, const double2 *tw, double nq, const Sink &sink) {
     constexpr int NC = 1 << LGC, NT = NC / kE, R = 1 << R_LOG, T0 = 1 << T0_LOG;
     const int tid = threadIdx.x;
 #pragma unroll
@@ -265,17 +284,23 @@ EPHDC_D void dit_pass_f64(double *buf, const Load &load, const double2 *tw, doub
         }
         dit_substages_f64<T0_LOG, R_LOG, 0>(x, tw, off, nq);
 #pragma unroll
-        for (int k = 0; k < R; ++k) buf[pad(base + k * T0)] = x[k];
+        for (int k = 0; k < R; ++k) {
+            if constexpr (SINK) sink(base + k * T0, x[k]);
+            else buf[pad(base + k * T0)] = x[k];
+        }
     }
-    __syncthreads();
+    if constexpr (!SINK) {
+        if constexpr (inv_warp_local<LGC, T0_LOG, R_LOG>() && inv_next_warp_local<LGC, T0_LOG>()) __syncwarp();
+        else __syncthreads();
+    }
 }
 
-template <int LGC, int DONE, bool FIRST, class Load>
-EPHDC_D void inv_dit_f64(double *buf, const Load &load, const double2 *tw, double nq) {
+template <int LGC, int DONE, bool FIRST, class Load, class Sink>
+EPHDC_D void inv_dit_f64(double *buf, const Load &load, const double2 *tw, double nq, const Sink &sink) {
     if constexpr (DONE < LGC) {
         constexpr int R_LOG = (LGC - DONE) >= 4 ? 4 : (LGC - DONE);
-        dit_pass_f64<LGC, DONE, R_LOG, FIRST>(buf, load, tw, nq);
-        inv_dit_f64<LGC, DONE + R_LOG, false>(buf, load, tw, nq);
+        dit_pass_f64<LGC, DONE, R_LOG, FIRST, DONE + R_LOG == LGC>(buf, load, tw, nq, sink);
+        inv_dit_f64<LGC, DONE + R_LOG, false>(buf, load, tw, nq, sink);
     }
 }
 
