@@ -470,6 +470,9 @@ ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_w
         const size_t per = D * c->N * sizeof(uint32_t);
         const size_t cap = std::max<size_t>(1, (32ull << 30) / per);
         ws->m_batches = (uint32_t)std::min<size_t>(std::min<size_t>(ws->nb_max, cap), 65535);
+        // test knob: smaller batch groups exercise the grouped path (taken above 32 GB)
+        if (const char *e = getenv("EPHDC_M_BATCHES"))
+            ws->m_batches = std::max<uint32_t>(1, std::min<uint32_t>(ws->m_batches, (uint32_t)atoi(e)));
     }
     if (dev_alloc(&ws->d_M, D * c->N * ws->m_batches) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
         dev_alloc(&ws->d_H, D * max_nq) != cudaSuccess ||

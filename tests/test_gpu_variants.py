@@ -75,3 +75,25 @@ def test_plan_variants_bit_identical(name, extra):
     for env in VARIANTS:
         got = _run(ps, ws, H, nq, env)
         assert np.array_equal(got, ref), env
+
+
+@pytest.mark.parametrize("name,groups", [("c3", "2"), ("c4", "7")])
+def test_batch_groups_bit_identical(name, groups):
+    """The FP64 path packs and evaluates the batches of a call in groups of at most
+    m_batches (the plaintext workspace is capped at 32 GB; c4 beyond ~50 batches):
+    grouping changes only the launch boundaries, never the ciphertexts."""
+    cfg = inp.CONFIGS[name]
+    Xtr, ytr, Xq, _ = inp.gen_features(cfg)
+    P = inp.gen_projection(cfg)
+    ps = ppipe.build(cfg, P, Xtr, ytr)
+    nq = 5 * ps.ctx.B + 11 if name == "c3" else 15 * ps.ctx.B + 7
+    X = torch.from_numpy(np.ascontiguousarray(Xq[:nq]).view(np.int8)).cuda()
+    H = eph.encode_queries(ps.ctx, X, ps.P_dev)
+    ref = eph.infer_batch(ps.ctx, ps.model, eph.Workspace(ps.ctx, nq), H, nq).cpu().numpy()
+    os.environ["EPHDC_M_BATCHES"] = groups
+    try:
+        ws = eph.Workspace(ps.ctx, nq)         # the knob is read when the workspace is made
+    finally:
+        os.environ.pop("EPHDC_M_BATCHES", None)
+    got = eph.infer_batch(ps.ctx, ps.model, ws, H, nq).cpu().numpy()
+    assert np.array_equal(got, ref)
