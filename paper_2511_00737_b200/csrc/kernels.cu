@@ -437,7 +437,18 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(u64 *__
             p[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
         }
     } else {
-        inv_ntt<u64, LG, E>(buf, load, tw, q, N + s * NC);
+        // the first inverse pass groups E consecutive residues per thread: stage the
+        // slice through shared memory with coalesced loads instead of reading that
+        // pattern from global memory (32x the L1 wavefronts); the pass then reads and
+        // rewrites only its own positions
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int pos = threadIdx.x + e * NT;
+            buf[pad(pos)] = p[pos];
+        }
+        __syncthreads();
+        auto sload = [&](int pos) -> u64 { return buf[pad(pos)]; };
+        inv_ntt<u64, LG, E>(buf, sload, tw, q, N + s * NC);
         if (S == 1) {
             const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
 #pragma unroll

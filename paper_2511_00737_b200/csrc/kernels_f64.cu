@@ -406,11 +406,19 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
                 __stcs(reinterpret_cast<ulonglong2 *>(o + 2 * g), v);
             }
         } else {
-            // the first inverse pass reads 16 consecutive residues per thread (lanes 128 B
-            // apart): L1-allocating loads so each 32-byte sector is fetched once
-            auto load = [&](int pos) -> double {
-                return centered(__ldg(reinterpret_cast<const unsigned long long *>(p + pos)));
-            };
+            // the first inverse pass groups 16 consecutive residues per thread (lanes 128 B
+            // apart): stage the polynomial through shared memory with coalesced loads
+            // instead (32x fewer L1 wavefronts than loading that pattern from global)
+            {
+                constexpr int NT = NC / kE;
+#pragma unroll
+                for (int e = 0; e < kE; ++e) {
+                    const int pos = tid + e * NT;
+                    buf[pad(pos)] = centered(__ldcs(reinterpret_cast<const unsigned long long *>(p + pos)));
+                }
+                __syncthreads();
+            }
+            auto load = [&](int pos) -> double { return buf[pad(pos)]; };
             // the last pass scales and stores straight to global memory (its lanes hold
             // consecutive positions: coalesced)
             auto sink = [&](int pos, double x) {
@@ -418,8 +426,8 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
                 const double y = reduce(mul_tw(x, c.x, c.y, nq), qinv, nq);
                 __stcs(reinterpret_cast<unsigned long long *>(p + pos), (unsigned long long)to_canonical_u64(y, q));
             };
-            if constexpr (DIR == 2) inv_dit_f64<LGC, 0, true>(buf, load, tw, nq, sink);
-            else inv_ntt_f64<LGC, 0, true>(buf, load, tw, nq, sink);
+            if constexpr (DIR == 2) inv_dit_f64<LGC, 0, false>(buf, load, tw, nq, sink);
+            else inv_ntt_f64<LGC, 0, false>(buf, load, tw, nq, sink);
         }
         __syncthreads();   // buf is rewritten by the next polynomial
     }
