@@ -392,14 +392,17 @@ __global__ void __launch_bounds__((1 << LGC) / kE, 1) k_ntt_std_f64(u64 *__restr
                 }
             };
             auto none = [] {};
-            fwd_ntt_head<LGC>(buf, load, tw, nq, after_first, none);
+            // NC = 2^13: the windowed tail (WL 2: the last head pass ends with
+            // __syncwarp); the lanes still store consecutive 16-byte pairs
+            constexpr int WLS = LGC == 13 ? 2 : 1;
+            fwd_ntt_head<LGC, WLS>(buf, load, tw, nq, after_first, none);
             u64 *o = p + (size_t)s * NC;
 #pragma unroll
             for (int u = 0; u < kE / 2; ++u) {
-                const int g = tail_pair<LGC, false>(u);
+                const int g = tail_pair<LGC, WLS == 2>(u);
                 const double2 w = tw[NC / 2 + g];
                 double x0, x1;
-                fwd_ntt_tail<LGC, false>(buf, u, w.x, w.y, nq, x0, x1);
+                fwd_ntt_tail<LGC, WLS == 2>(buf, u, w.x, w.y, nq, x0, x1);
                 ulonglong2 v;
                 v.x = to_canonical_u64(reduce(x0, qinv, nq), q);
                 v.y = to_canonical_u64(reduce(x1, qinv, nq), q);
