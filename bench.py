@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--plan", default="", help="A/B only: workspace launch-plan overrides, e.g. 'flags=2,bg=8'")
     return ap.parse_args()
 
 
@@ -199,7 +200,8 @@ def main():
     nq = cfg.nq
     nb = ctx.n_batches(nq)
     X_dev = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).to(dev)
-    ws = eph.Workspace(ctx, nq)
+    plan = {k: int(v, 0) for k, v in (kv.split("=") for kv in a.plan.split(",") if kv)} or None
+    ws = eph.Workspace(ctx, nq, plan=plan)
     H = torch.empty((cfg.D_live, nq), dtype=torch.int8, device=dev)
     out = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)

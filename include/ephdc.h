@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define EPHDC_ABI_VERSION 1
+#define EPHDC_ABI_VERSION 2
 #define EPHDC_MAX_PRIMES 16
 
 typedef enum {
@@ -103,6 +103,21 @@ typedef struct {
     uint32_t arith;          /* selected pipe: EPHDC_ARITH_INT or EPHDC_ARITH_F64 */
     uint32_t f64_red_every;  /* FP64 path: accumulator reduction interval (dims) */
 } ephdc_ctx_info;
+
+/* TEST / PROFILING launch-plan overrides of a workspace (ephdc_workspace_create;
+ * NULL or all zeros = the tuned plan).  Results are bit-identical for every value
+ * (tests/test_gpu_variants.py); nothing else -- no environment variable -- changes a
+ * launch plan. */
+typedef struct {
+    uint32_t flags;      /* FP64 fused kernel: bits 1-2 = 1/2/3 force the pass
+                          * synchronisation WL = 0/2/1; bit 0 = no L2 prefetch of the
+                          * model slice, bit 4 = prefetch; bit 3 = 32 elements per
+                          * thread (NC = 2^13)                                        */
+    uint32_t bg;         /* FP64 fused kernel: batches per group (0 = planner)       */
+    uint32_t G;          /* FP64 fused kernel: dims per chunk (0 = planner)          */
+    uint32_t m_batches;  /* batches of encoded plaintexts kept (0 = planner: all of
+                          * max_nq, capped at 32 GB)                                 */
+} ephdc_plan;
 
 typedef struct ephdc_ctx ephdc_ctx;
 typedef struct ephdc_sk ephdc_sk;
@@ -184,8 +199,12 @@ ephdc_status ephdc_model_scale(const ephdc_ctx *ctx, ephdc_model *model, uint32_
 /* ---------------- client side (the hot path; CS2) ---------------------------- */
 
 /* Device scratch for up to max_nq queries: query/hypervector staging, the
- * encoded plaintexts of one batch and the scores buffers.  Synchronous. */
-ephdc_status ephdc_workspace_create(const ephdc_ctx *ctx, uint32_t max_nq, ephdc_workspace **out);
+ * encoded plaintexts (FP64 path: of every batch of the call, up to 32 GB) and the
+ * scores buffers.  plan: launch-plan overrides for tests/profiling (ephdc_plan;
+ * NULL = the tuned plan).  Synchronous.  Errors: ENULL, ECONTEXT (host-only
+ * context), EPARAM (max_nq = 0), ERESOURCE. */
+ephdc_status ephdc_workspace_create(const ephdc_ctx *ctx, uint32_t max_nq, const ephdc_plan *plan,
+                                    ephdc_workspace **out);
 void ephdc_workspace_free(ephdc_workspace *ws);
 /* Per-kernel-class device time (ms, CUDA events on the launching stream) of
  * the calls since the last reset, when timing is enabled.  names/ms/launches
@@ -243,7 +262,8 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *ctx, const ephdc_model *model,
  * ciphertexts per batch instead of one). */
 
 /* Client: batch b of d_H [D_live][nq] -> d_qct [D_live][L][2][N]: secret-key BFV with
- * the client's key (readings #4-#10), random streams of ciphertext index b*D_live + d.
+ * the client's key (readings #4-#10), random streams of ciphertext index 2^32 + b*D_live + d (#25: disjoint from the model's
+ * indices d < D_live, so query and model ciphertexts never share a or e).
  * Uses the workspace's plaintext buffer.  Async. */
 ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *ctx, ephdc_sk *sk, ephdc_workspace *ws, const int8_t *d_H,
                                       uint32_t nq, uint32_t b, uint64_t seed, uint64_t *d_qct, void *stream);
@@ -271,10 +291,11 @@ ephdc_status ephdc_pack_scores(const ephdc_ctx *ctx, const uint64_t *d_ct, uint3
 ephdc_status ephdc_unpack_scores(const ephdc_ctx *ctx, const uint8_t *h_msg, uint32_t nb, uint64_t *h_ct);
 /* End-to-end client call producing the message: h_X -> device, encode_queries +
  * infer_batch + pack_scores, message -> h_msg (ephdc_scores_message_bytes(ctx, nb)
- * bytes).  Synchronous on `stream`. */
+ * bytes; cap_bytes = capacity of h_msg, EOVERFLOW if smaller, nothing written).
+ * Synchronous on `stream`. */
 ephdc_status ephdc_classify_host_packed(const ephdc_ctx *ctx, const ephdc_model *model, ephdc_workspace *ws,
                                         const void *h_X, const int8_t *d_P, uint32_t nq, uint8_t *h_msg,
-                                        void *stream);
+                                        size_t cap_bytes, void *stream);
 
 /* ---------------- server decide (test-only host; CS3) ----------------------- */
 
@@ -308,9 +329,14 @@ ephdc_status ephdc_noise_probe(const ephdc_ctx *ctx, const ephdc_sk *sk, const u
 /* ---------------- standalone kernels (c5 microbench; CS5) ------------------- */
 
 /* Tables for L primes (each = 1 mod 2N, < 2^61) at ring degree N = 2^log2N,
- * 10 <= log2N <= 16, on `device`.  Synchronous. */
+ * 10 <= log2N <= 16, on `device`.  flags: 0 = the tuned kernels (FP64 pipe where
+ * the bounds of DESIGN.md 5.1 hold, else the integer pipe); EPHDC_NTT_FORCE_INT =
+ * the integer-pipe kernels everywhere (TEST/PROFILING: bit-identical results).
+ * Synchronous.  Errors: ENULL, EPARAM (sizes, a q_j that is not an NTT prime, unknown
+ * flags), ECONTEXT (device < 0), ECUDA, ERESOURCE. */
+#define EPHDC_NTT_FORCE_INT 1u
 ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device,
-                                   ephdc_ntt_plan **out);
+                                   uint32_t flags, ephdc_ntt_plan **out);
 void ephdc_ntt_plan_free(ephdc_ntt_plan *p);
 /* In-place negacyclic NTT of d_polys [batch][L][N] (residues < q_j), natural
  * coefficient order <-> bit-reversed evaluation order (#1).  Async. */

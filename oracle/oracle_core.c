@@ -439,7 +439,8 @@ void or_decrypt_phase(const or_bfv *P, const u64 *ct, u64 *out) {
 
 /* query ciphertexts of batch b, dims [d0, d0+nd): out[nd][L][2][N]; message = the query
    slot vector of (b, d) encoded mod t ([0,t), Delta*m as for the model, reading #4);
-   random streams of ciphertext index g = b*D_live + d. */
+   random streams of ciphertext index g = 2^32 + b*D_live + d (DESIGN reading #25: an index
+   space disjoint from the model's d < D_live). */
 void or_encrypt_queries(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0, u32 nd, u64 *out) {
     u32 N = 1u << P->logN;
     u64 *tinv = (u64 *)malloc(sizeof(u64) * N);
@@ -454,7 +455,7 @@ void or_encrypt_queries(const or_bfv *P, const int8_t *H, u32 nq, u32 b, u32 d0,
         for (long long dd = 0; dd < (long long)nd; ++dd) {
             u32 d = d0 + (u32)dd;
             query_plaintext(P, H, nq, b, d, tinv, m);
-            encrypt_msg(P, (u64)b * P->D_live + d, m, fw, e, x, out + (u64)dd * P->L * 2 * N);
+            encrypt_msg(P, (1ULL << 32) + (u64)b * P->D_live + d, m, fw, e, x, out + (u64)dd * P->L * 2 * N);
         }
         free(m); free(x); free(e);
     }

@@ -178,11 +178,19 @@ class EncryptedModel:
 
 
 class Workspace:
-    def __init__(self, ctx: Context, max_nq: int):
+    """ephdc_workspace.  plan: TEST/PROFILING launch-plan overrides {"flags", "bg", "G",
+    "m_batches"} (ephdc_plan; None = the tuned plan, results bit-identical)."""
+
+    def __init__(self, ctx: Context, max_nq: int, plan: Optional[Dict[str, int]] = None):
         self.ctx = ctx
         self.max_nq = max_nq
+        pl = dict(plan or {})
+        unknown = set(pl) - {"flags", "bg", "G", "m_batches"}
+        if unknown:
+            raise ValueError(f"unknown plan overrides {sorted(unknown)}")
+        self._plan = _capi.Plan(pl.get("flags", 0), pl.get("bg", 0), pl.get("G", 0), pl.get("m_batches", 0))
         self._h = ctypes.c_void_p()
-        call("ephdc_workspace_create", ctx.handle, max_nq, ctypes.byref(self._h))
+        call("ephdc_workspace_create", ctx.handle, max_nq, ctypes.byref(self._plan), ctypes.byref(self._h))
 
     @property
     def handle(self):
@@ -320,7 +328,7 @@ def classify_host_packed(ctx: Context, model: EncryptedModel, ws: Workspace, X_h
     if msg_host is None:
         msg_host = torch.empty(scores_message_bytes(ctx, ctx.n_batches(nq)), dtype=torch.uint8, pin_memory=True)
     call("ephdc_classify_host_packed", ctx.handle, model.handle, ws.handle, X_host.data_ptr(), _dptr(P), nq,
-         msg_host.data_ptr(), _stream(stream))
+         msg_host.data_ptr(), msg_host.numel(), _stream(stream))
     return msg_host
 
 
@@ -355,12 +363,16 @@ def noise_probe(ctx: Context, sk: SecretKey, cts, stream=None) -> Tuple[np.ndarr
 
 # --------------------------------------------------------------------------- standalone (c5)
 class NttPlan:
-    def __init__(self, q: Sequence[int], log2N: int, device: int = 0):
+    """ephdc_ntt_plan.  force_int: the integer-pipe kernels everywhere (tests/profiling,
+    EPHDC_NTT_FORCE_INT; bit-identical results)."""
+
+    def __init__(self, q: Sequence[int], log2N: int, device: int = 0, force_int: bool = False):
         self.q = [int(x) for x in q]
         self.L, self.log2N, self.N = len(q), log2N, 1 << log2N
         qa = np.ascontiguousarray(np.array(self.q, dtype=np.uint64))
         self._h = ctypes.c_void_p()
-        call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device, ctypes.byref(self._h))
+        call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device, 1 if force_int else 0,
+             ctypes.byref(self._h))
 
     @property
     def handle(self):

@@ -10,8 +10,7 @@ import os
 from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# EPHDC_LIB: an alternative build of the same library (A/B experiments, tools/ab_libs.sh)
-LIB_PATH = os.environ.get("EPHDC_LIB") or os.path.join(HERE, "libephdc.so")
+LIB_PATH = os.path.join(HERE, "libephdc.so")
 
 MAX_PRIMES = 16
 
@@ -38,6 +37,10 @@ class Params(ctypes.Structure):
 
 
 ARITH_AUTO, ARITH_INT, ARITH_F64 = 0, 1, 2
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("flags", c_u32), ("bg", c_u32), ("G", c_u32), ("m_batches", c_u32)]
 
 
 class CtxInfo(ctypes.Structure):
@@ -67,7 +70,7 @@ _SIGS = {
     "ephdc_model_free": (None, [c_vp]),
     "ephdc_model_export": (c_st, [c_vp, c_u32, c_u32, c_vp]),
     "ephdc_model_scale": (c_st, [c_vp, c_vp, c_u32, c_vp, c_u32]),
-    "ephdc_workspace_create": (c_st, [c_vp, c_u32, c_vp]),
+    "ephdc_workspace_create": (c_st, [c_vp, c_u32, c_vp, c_vp]),
     "ephdc_workspace_free": (None, [c_vp]),
     "ephdc_workspace_set_timing": (c_st, [c_vp, c_int]),
     "ephdc_workspace_timing": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp]),
@@ -83,10 +86,10 @@ _SIGS = {
     "ephdc_scores_message_bytes": (ctypes.c_size_t, [c_vp, c_u32]),
     "ephdc_pack_scores": (c_st, [c_vp, c_vp, c_u32, c_vp, c_vp]),
     "ephdc_unpack_scores": (c_st, [c_vp, c_vp, c_u32, c_vp]),
-    "ephdc_classify_host_packed": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
+    "ephdc_classify_host_packed": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, ctypes.c_size_t, c_vp]),
     "ephdc_decrypt_slots": (c_st, [c_vp, c_vp, c_vp, c_vp]),
     "ephdc_noise_probe": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
-    "ephdc_ntt_plan_create": (c_st, [c_vp, c_u32, c_u32, c_int, c_vp]),
+    "ephdc_ntt_plan_create": (c_st, [c_vp, c_u32, c_u32, c_int, c_u32, c_vp]),
     "ephdc_ntt_plan_free": (None, [c_vp]),
     "ephdc_ntt_fwd": (c_st, [c_vp, c_vp, c_u32, c_vp]),
     "ephdc_ntt_inv": (c_st, [c_vp, c_vp, c_u32, c_vp]),

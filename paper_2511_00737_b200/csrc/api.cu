@@ -220,7 +220,6 @@ ephdc_status ephdc_ctx_create(const ephdc_params *p, int device, ephdc_ctx **out
         const bool ok = plan_f64(c->q, p->t, p->log2N, &c->f64);
         if (!ok && p->arith == EPHDC_ARITH_F64) return EPHDC_EPARAM;
     }
-    if (const char *e = getenv("EPHDC_F64_FLAGS")) c->f64_flags_env = (uint32_t)strtoul(e, nullptr, 0);
     c->device = device;
     if (device >= 0) {
         int ndev = 0;
@@ -342,14 +341,7 @@ ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_
     return EPHDC_OK;
 }
 
-void ephdc_model_free(ephdc_model *m) {
-    if (!m) return;
-    if (m->d_ct) {
-        cudaSetDevice(m->ctx->device);
-        cudaFree(m->d_ct);
-    }
-    delete m;
-}
+void ephdc_model_free(ephdc_model *m) { delete m; }   // ~ephdc_model frees d_ct
 
 ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const int8_t *class_hv, uint64_t seed,
                                  ephdc_model **out) {
@@ -451,7 +443,8 @@ void ephdc_workspace_free(ephdc_workspace *ws) {
     delete ws;
 }
 
-ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_workspace **out) {
+ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, const ephdc_plan *plan,
+                                    ephdc_workspace **out) {
     if (!c || !out) return EPHDC_ENULL;
     *out = nullptr;
     if (c->device < 0) return EPHDC_ECONTEXT;
@@ -461,6 +454,7 @@ ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_w
     if (!ws) return EPHDC_ERESOURCE;
     ws->ctx = c;
     ws->max_nq = max_nq;
+    if (plan) ws->plan = *plan;
     ws->nb_max = (max_nq + c->B - 1) / c->B;
     const size_t D = c->p.D_live;
     // FP64 path: the encoded plaintexts of all batches are kept (one fused launch over
@@ -470,9 +464,8 @@ ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, ephdc_w
         const size_t per = D * c->N * sizeof(uint32_t);
         const size_t cap = std::max<size_t>(1, (32ull << 30) / per);
         ws->m_batches = (uint32_t)std::min<size_t>(std::min<size_t>(ws->nb_max, cap), 65535);
-        // test knob: smaller batch groups exercise the grouped path (taken above 32 GB)
-        if (const char *e = getenv("EPHDC_M_BATCHES"))
-            ws->m_batches = std::max<uint32_t>(1, std::min<uint32_t>(ws->m_batches, (uint32_t)atoi(e)));
+        // plan override (tests): smaller batch groups exercise the grouped path (taken above 32 GB)
+        if (ws->plan.m_batches) ws->m_batches = std::min<uint32_t>(ws->m_batches, ws->plan.m_batches);
     }
     if (dev_alloc(&ws->d_M, D * c->N * ws->m_batches) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
         dev_alloc(&ws->d_H, D * max_nq) != cudaSuccess ||
@@ -563,7 +556,7 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
             }
             {
                 Timer tm(ws, st, kClsMac);
-                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->d_M, g, reinterpret_cast<const double *>(m->d_ct), d_out + per * b0, st));
+                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->plan, ws->d_M, g, reinterpret_cast<const double *>(m->d_ct), d_out + per * b0, st));
                 tm.done();
             }
         }
@@ -655,7 +648,8 @@ ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *c, ephdc_sk *sk, ephdc_wo
     }
     const uint32_t D = c->p.D_live;
     EPHDC_CUDA_TRY(launch_pack_intt_sr(c, d_H, false, nq, b, 0, D, ws->d_M, st));
-    EPHDC_CUDA_TRY(launch_encrypt(c, ws->d_M, b * D, D, sk->d_shat_mont, seed, d_qct, st));
+    // stream indices 2^32 + b*D + d: disjoint from the model's d < D_live (reading #25)
+    EPHDC_CUDA_TRY(launch_encrypt(c, ws->d_M, (1ull << 32) + (uint64_t)b * D, D, sk->d_shat_mont, seed, d_qct, st));
     return EPHDC_OK;
 }
 
@@ -728,12 +722,13 @@ ephdc_status ephdc_unpack_scores(const ephdc_ctx *c, const uint8_t *h_msg, uint3
 
 ephdc_status ephdc_classify_host_packed(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws,
                                         const void *h_X, const int8_t *d_P, uint32_t nq, uint8_t *h_msg,
-                                        void *stream) {
+                                        size_t cap_bytes, void *stream) {
     if (!c || !m || !ws || ((!h_X || !d_P || !h_msg) && nq)) return EPHDC_ENULL;
     if (m->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
     if (nq > ws->max_nq) return EPHDC_EPARAM;
     if (nq == 0) return EPHDC_OK;
     const uint32_t nb = (nq + c->B - 1) / c->B;
+    if (cap_bytes < ephdc_scores_message_bytes(c, nb)) return EPHDC_EOVERFLOW;
     EPHDC_CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
     EPHDC_CUDA_TRY(cudaMemcpyAsync(ws->d_X, h_X, (size_t)nq * c->p.F, cudaMemcpyHostToDevice, st));
@@ -827,10 +822,11 @@ void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
     delete p;
 }
 
-ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device, ephdc_ntt_plan **out) {
+ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device, uint32_t flags,
+                                   ephdc_ntt_plan **out) {
     if (!q || !out) return EPHDC_ENULL;
     *out = nullptr;
-    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16) return EPHDC_EPARAM;
+    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16 || (flags & ~EPHDC_NTT_FORCE_INT)) return EPHDC_EPARAM;
     for (uint32_t j = 0; j < L; ++j)
         if (q[j] >= (1ull << 61) || !is_ntt_prime(q[j], log2N)) return EPHDC_EPARAM;
     if (device < 0) return EPHDC_ECONTEXT;
@@ -858,9 +854,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
         ninv[2 * j + 1] = shoup64(ninv[2 * j], q[j]);
     }
     plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
-    if (const char *e = getenv("EPHDC_NTT_INT")) {  // profiling knob: force the integer kernels
-        if (atoi(e)) p->fwd_f64 = p->inv_f64 = false;
-    }
+    if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
     if (p->fwd_f64 || p->inv_f64) {
         // FP64 tables: forward psi_rev; inverse = Cooley-Tukey DIT on the bit-reversed
         // input (x[r] = DFT(a psi^j)[brev r]): stage of half-size h uses omega^-(N/2h) jj

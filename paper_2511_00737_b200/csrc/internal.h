@@ -71,7 +71,6 @@ struct ephdc_ctx {
     ephdc::ctxDev dev;
     uint32_t fused_S = 1, fused_chunks = 1, fused_G = 1;
     ephdc::F64Plan f64;
-    uint32_t f64_flags_env = 0;    // EPHDC_F64_FLAGS (profiling knobs, read at ctx creation)
     std::vector<uint32_t> qbits;   // bit_length(q_j): scores-message packing widths
 };
 
@@ -86,6 +85,15 @@ struct ephdc_model {
     const ephdc_ctx *ctx = nullptr;
     uint64_t *d_ct = nullptr;     // [D_live][L][2][N]: u64 (integer path) or exact doubles (FP64 path)
     uint32_t D = 0;
+    ephdc_model() = default;
+    ephdc_model(const ephdc_model &) = delete;
+    ephdc_model &operator=(const ephdc_model &) = delete;
+    ~ephdc_model() {  // owns d_ct: every error path of ephdc_encrypt_model releases it
+        if (d_ct) {
+            cudaSetDevice(ctx->device);
+            cudaFree(d_ct);
+        }
+    }
 };
 
 struct ephdc_workspace {
@@ -98,6 +106,7 @@ struct ephdc_workspace {
     uint64_t *d_out = nullptr;    // [nb_max][2][L][N]
     uint8_t *d_msg = nullptr;     // packed scores message of nb_max ciphertexts
     uint32_t nb_max = 0;
+    ephdc_plan plan{};            // launch-plan overrides (tests/profiling; zeros = tuned)
     // timing
     bool timing = false;
     static constexpr int kClasses = 4;
@@ -144,7 +153,7 @@ cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32
                                  cudaStream_t st);
 // secret-key encryption of nd encoded messages d_M ([0, t)): random streams g0 + dd,
 // output d_out [nd][L][2][N]
-cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t g0, uint32_t nd,
+cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint64_t g0, uint32_t nd,
                            const uint64_t *d_shat_mont, uint64_t seed, uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_pack_intt_sr(const ephdc_ctx *c, const int8_t *src, bool model, uint32_t nq, uint32_t b,
                                 uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st);
@@ -160,8 +169,8 @@ bool encode_tc_supported(const ephdc_ctx *c);
 cudaError_t launch_encode_tc(const ephdc_ctx *c, const void *d_X, const int8_t *d_P, uint32_t nq, void *d_H, bool raw,
                              cudaStream_t st);
 // FP64-pipe path (kernels_f64.cu)
-cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
-                               uint64_t *d_out, cudaStream_t st);
+cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const ephdc_plan &plan, const uint32_t *d_M, uint32_t nb,
+                               const double *d_model, uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st);
 // scores message layout (bit-packed residues, ephdc.h "scores message")
 struct MsgLayout {

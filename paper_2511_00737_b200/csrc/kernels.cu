@@ -206,7 +206,8 @@ EPHDC_D void inv_passes_perm(u32 *buf, const Load &load, const TwPair<u32> *tw, 
 // A CTA keeps the whole psi_t^-1 table in shared memory in the pass-major layout (the
 // lanes of a warp read consecutive 8-byte pairs: conflict-free) and loops over rows
 // with stride gridDim.x; the slot -> query division i / k is a multiply-high by
-// m = floor(2^32 / k) + 1 (exact for i < 2^16, k <= 2^16).  Output: centered int32.
+// m = floor(2^32 / k) + 1 (exact for i < 2^16, 2 <= k <= 2^16; k = 1 is the identity,
+// whose multiplier 2^32 + 1 does not fit 32 bits).  Output: centered int32.
 // =====================================================================================
 template <int LG>
 __global__ void __launch_bounds__((1 << LG) / kE, (LG >= 14) ? 1 : (16384 >> LG))
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__((1 << LG) / kE, (LG >= 14) ? 1 : (16384 >> LG)
         const int8_t *src = H + (size_t)d * nq + (size_t)b * a.B;
         auto load = [&](int i) -> u32 {
             if ((u32)i >= lim) return 0u;
-            const int v = src[__umulhi((u32)i, kmagic)];
+            const int v = src[k == 1u ? (u32)i : __umulhi((u32)i, kmagic)];
             return v < 0 ? (u32)((int)t + v) : (u32)v;
         };
         inv_passes_perm<LG, 0, true>(buf, load, tw, t, two_t);
@@ -366,14 +367,15 @@ struct EncArgs {
 
 template <int LG>
 __global__ void __launch_bounds__((1 << LG) / kE)
-    k_encrypt(const u32 *__restrict__ M, u32 g0, EncArgs a, u64 *__restrict__ out) {
+    k_encrypt(const u32 *__restrict__ M, u64 g0, EncArgs a, u64 *__restrict__ out) {
     constexpr int N = 1 << LG, NT = N / kE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
     __shared__ u64 cdt[ephdc_rng::kCdtLen];
     if (threadIdx.x < ephdc_rng::kCdtLen) cdt[threadIdx.x] = a.cdt[threadIdx.x];
     __syncthreads();
-    const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L, d = g0 + dd;   // d: random-stream index
+    const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L;
+    const u64 d = g0 + dd;   // random-stream index (model: d; HE-HDC-SR queries: 2^32 + b D + d)
     const u64 q = a.ps.q[j], delta = a.ps.delta[j], delta_p = a.ps.delta_p[j];
     const u32 *m = M + (size_t)dd * N;
     const u64 seed = a.seed;
@@ -625,7 +627,7 @@ static cudaError_t packq_launch(const ephdc_ctx *c, const int8_t *H, u32 nq, u32
     const int per_sm = LG >= 14 ? 1 : (16384 >> LG);
     const uint64_t rows = (uint64_t)nbat * D;
     const u32 grid = (u32)std::min<uint64_t>(rows, 148ull * per_sm);
-    const u32 kmagic = (u32)((1ull << 32) / c->p.k + 1);
+    const u32 kmagic = c->p.k > 1 ? (u32)((1ull << 32) / c->p.k + 1) : 0u;   // k = 1: identity
     kern<<<grid, (1 << LG) / kE, smem, st>>>(H, nq, b0, nbat, D, pack_args(c), kmagic, M);
     return counted(cudaGetLastError());
 }
@@ -736,7 +738,7 @@ cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32
 }
 
 template <int LG>
-static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u32 d0, u32 nd, const u64 *shat, u64 seed, u64 *model,
+static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u64 d0, u32 nd, const u64 *shat, u64 seed, u64 *model,
                               cudaStream_t st) {
     const size_t smem = sizeof(u64) * padded_len(1 << LG);
     auto kern = k_encrypt<LG>;
@@ -753,7 +755,7 @@ static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u32 d0, u32 nd, 
     return counted(cudaGetLastError());
 }
 
-cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t d0, uint32_t nd,
+cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint64_t d0, uint32_t nd,
                            const uint64_t *d_shat_mont, uint64_t seed, uint64_t *d_model, cudaStream_t st) {
     if (nd == 0) return cudaSuccess;
     switch (c->p.log2N) {

@@ -651,19 +651,18 @@ template <class K> static cudaError_t smem_attr(K kernel, size_t bytes) {
 }
 
 template <int LGC, int S>
-static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb, const double *model, u64 *out,
-                                  cudaStream_t st) {
+static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, const u32 *M, uint32_t nb,
+                                  const double *model, u64 *out, cudaStream_t st) {
     // pad shared memory so that no more CTAs share an SM than its TMEM holds
     const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
     // Plan (profiles/r01/ab_wl2.txt): at NC = 2^13 the windowed tail (WL = 2: the last
     // head pass ends with __syncwarp, 2 CTA barriers per dim) without the explicit L2
     // prefetch of the model slice is fastest (c4 -5.5%, c3 -1.6%); smaller transforms
     // keep WL = 1 with the prefetch (c2: WL = 2 is 20% slower).
-    // EPHDC_F64_FLAGS (profiling knob, read per launch) overrides: bits 1-2 = 1/2/3 force
+    // ephdc_plan.flags (workspace plan overrides, tests/profiling): bits 1-2 = 1/2/3 force
     // WL = 0/2/1; bit 0 forces the prefetch off, bit 4 on; bit 3 = 32 elements per
     // thread (LGC = 13 only; WL = 2 or 1).
-    u32 env = c->f64_flags_env;
-    if (const char *ev = getenv("EPHDC_F64_FLAGS")) env = (u32)strtoul(ev, nullptr, 0);
+    const u32 env = plan.flags;
     u32 wl = LGC >= 13 ? 2u : 1u;
     bool prefetch = LGC < 13;
     switch ((env >> 1) & 3u) {
@@ -683,11 +682,11 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
     a.nb = nb;
     f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
     a.flags = prefetch ? 0u : 1u;  // bit 0: no explicit L2 prefetch of the model slice
-    // experiment knobs (profiling only; defaults are the tuned plan)
-    if (const char *e = getenv("EPHDC_F64_BG")) a.bg = std::max<u32>(1, std::min<u32>(nb, (u32)strtoul(e, nullptr, 0)));
-    if (const char *e = getenv("EPHDC_F64_G")) {  // <= 1024 chunks: the 64-bit fold of f64_grid
+    // plan overrides (ephdc_plan bg / G; tests and profiling only)
+    if (plan.bg) a.bg = std::max<u32>(1, std::min<u32>(nb, plan.bg));
+    if (plan.G) {  // <= 1024 chunks: the 64-bit fold of f64_grid
         const u32 gmin = (c->p.D_live + 1023) / 1024;
-        a.G = std::max<u32>(gmin, std::min<u32>(c->p.D_live, (u32)strtoul(e, nullptr, 0)));
+        a.G = std::max<u32>(gmin, std::min<u32>(c->p.D_live, plan.G));
         a.chunks = (c->p.D_live + a.G - 1) / a.G;
     }
     const uint64_t groups = (nb + a.bg - 1) / a.bg;
@@ -698,15 +697,15 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const u32 *M, uint32_t nb,
 }
 
 
-cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nb, const double *d_model,
-                               uint64_t *d_out, cudaStream_t st) {
+cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const ephdc_plan &plan, const uint32_t *d_M, uint32_t nb,
+                               const double *d_model, uint64_t *d_out, cudaStream_t st) {
     if (nb == 0) return cudaSuccess;
     switch (c->p.log2N) {
-        case 10: return mac_f64_launch<10, 1>(c, d_M, nb, d_model, d_out, st);
-        case 11: return mac_f64_launch<11, 1>(c, d_M, nb, d_model, d_out, st);
-        case 12: return mac_f64_launch<12, 1>(c, d_M, nb, d_model, d_out, st);
-        case 13: return mac_f64_launch<13, 1>(c, d_M, nb, d_model, d_out, st);
-        case 14: return mac_f64_launch<13, 2>(c, d_M, nb, d_model, d_out, st);
+        case 10: return mac_f64_launch<10, 1>(c, plan, d_M, nb, d_model, d_out, st);
+        case 11: return mac_f64_launch<11, 1>(c, plan, d_M, nb, d_model, d_out, st);
+        case 12: return mac_f64_launch<12, 1>(c, plan, d_M, nb, d_model, d_out, st);
+        case 13: return mac_f64_launch<13, 1>(c, plan, d_M, nb, d_model, d_out, st);
+        case 14: return mac_f64_launch<13, 2>(c, plan, d_M, nb, d_model, d_out, st);
     }
     return cudaErrorInvalidValue;
 }

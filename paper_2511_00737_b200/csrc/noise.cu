@@ -186,7 +186,7 @@ extern "C" ephdc_status ephdc_noise_probe(const ephdc_ctx *c, const ephdc_sk *sk
         }
 
     ephdc_ntt_plan *plan = nullptr;
-    ephdc_status s = ephdc_ntt_plan_create(c->q.data(), L, c->p.log2N, c->device, &plan);
+    ephdc_status s = ephdc_ntt_plan_create(c->q.data(), L, c->p.log2N, c->device, 0u, &plan);
     if (s != EPHDC_OK) return s;
     std::unique_ptr<ephdc_ntt_plan, void (*)(ephdc_ntt_plan *)> plan_guard(plan, ephdc_ntt_plan_free);
 

@@ -46,16 +46,19 @@ def gather_ciphertexts(local: np.ndarray, dst: int = 0) -> List[np.ndarray]:
     import torch
     import torch.distributed as dist
     world, rank = dist.get_world_size(), dist.get_rank()
+    # NCCL moves only CUDA tensors (over NVLink); gloo moves CPU tensors
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
     shape = list(local.shape)
-    n = torch.tensor([shape[0]], dtype=torch.int64)
-    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    n = torch.tensor([shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, n)
-    nmax = int(max(int(s.item()) for s in sizes))
+    counts = [int(s.item()) for s in sizes]
+    nmax = max(counts)
     pad = np.zeros([nmax] + shape[1:], dtype=np.uint64)
     pad[: shape[0]] = local
-    t = torch.from_numpy(pad.view(np.int64))
+    t = torch.from_numpy(pad.view(np.int64)).to(dev)
     bufs = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(bufs, t)   # gloo/NCCL both implement all_gather; NCCL has no gather
     if rank != dst:
         return []
-    return [b.numpy().view(np.uint64)[: int(sizes[r].item())] for r, b in enumerate(bufs)]
+    return [b.cpu().numpy().view(np.uint64)[: counts[r]] for r, b in enumerate(bufs)]

@@ -26,15 +26,13 @@ def _host(t):
 @pytest.mark.parametrize("force_int", [False, True])
 @pytest.mark.parametrize("log2N", [10, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("L,bits", [(1, 30), (3, 60), (5, 60), (9, 48), (16, 30), (16, 60)])
-def test_ntt_fwd_inv_bitexact(log2N, L, bits, force_int, monkeypatch):
-    # default: the FP64 kernels where the plan's bounds allow them (primes < 2^50,
-    # N <= 2^14 forward / 2^13 inverse), else the integer kernels; force_int: integer only
-    if force_int:
-        monkeypatch.setenv("EPHDC_NTT_INT", "1")
+def test_ntt_fwd_inv_bitexact(log2N, L, bits, force_int):
+    # default: the FP64 kernels where the plan's bounds allow them (primes < 2^50),
+    # else the integer kernels; force_int: integer only (EPHDC_NTT_FORCE_INT)
     q = nt.prime_chain([bits] * L, log2N)
     batch = 3
     x = inp.gen_residues(q, batch, 1 << log2N, seed=log2N * 100 + L)
-    plan = eph.NttPlan(q, log2N)
+    plan = eph.NttPlan(q, log2N, force_int=force_int)
     d = _dev(x)
     eph.ntt_fwd(plan, d)
     got = _host(d)

@@ -2,14 +2,12 @@
 
 The default plan (f64_grid + the WL / prefetch choice in mac_f64_launch) is checked
 against the oracle by test_gpu_fullsize / test_gpu_parity; every other variant the
-EPHDC_F64_* profiling knobs select must produce exactly the same scores ciphertexts:
+workspace plan overrides (ephdc_plan) select must produce exactly the same scores ciphertexts:
 the synchronisation variants WL = 0/1/2, 32 elements per thread, the explicit L2
 prefetch on/off, and other grid plans (batches per group, dims per chunk -- i.e. other
 orders of the 64-bit atomic folds, which integer addition makes order independent).
 Each variant's output also decrypts to the brute-force integer scores.
 """
-import os
-
 import numpy as np
 import pytest
 
@@ -25,33 +23,25 @@ if not torch.cuda.is_available():
 import paper_2511_00737_b200 as eph  # noqa: E402
 from paper_2511_00737_b200 import pipeline as ppipe  # noqa: E402
 
-KNOBS = ("EPHDC_F64_FLAGS", "EPHDC_F64_BG", "EPHDC_F64_G")
 VARIANTS = [
-    {"EPHDC_F64_FLAGS": "2"},            # WL = 0: a CTA barrier after every pass
-    {"EPHDC_F64_FLAGS": "6"},            # WL = 1
-    {"EPHDC_F64_FLAGS": "4"},            # WL = 2
-    {"EPHDC_F64_FLAGS": "16"},           # explicit L2 prefetch on
-    {"EPHDC_F64_FLAGS": "1"},            # explicit L2 prefetch off
-    {"EPHDC_F64_FLAGS": "8"},            # 32 elements per thread (NC = 2^13 only), planned WL
-    {"EPHDC_F64_FLAGS": "14"},           # 32 elements per thread, WL = 1
-    {"EPHDC_F64_FLAGS": "12"},           # 32 elements per thread, WL = 2
-    {"EPHDC_F64_BG": "1", "EPHDC_F64_G": "37"},
-    {"EPHDC_F64_BG": "2", "EPHDC_F64_G": "1000"},
+    {"flags": 2},            # WL = 0: a CTA barrier after every pass
+    {"flags": 6},            # WL = 1
+    {"flags": 4},            # WL = 2
+    {"flags": 16},           # explicit L2 prefetch on
+    {"flags": 1},            # explicit L2 prefetch off
+    {"flags": 8},            # 32 elements per thread (NC = 2^13 only), planned WL
+    {"flags": 14},           # 32 elements per thread, WL = 1
+    {"flags": 12},           # 32 elements per thread, WL = 2
+    {"bg": 1, "G": 37},
+    {"bg": 2, "G": 1000},
 ]
 
 
-def _run(ps, ws, H, nq, env):
-    saved = {k: os.environ.pop(k, None) for k in KNOBS}
-    try:
-        os.environ.update(env)
-        out = eph.infer_batch(ps.ctx, ps.model, ws, H, nq)
-        torch.cuda.synchronize()
-        return out.cpu().numpy().view(np.uint64).copy()
-    finally:
-        for k in KNOBS:
-            os.environ.pop(k, None)
-            if saved[k] is not None:
-                os.environ[k] = saved[k]
+def _run(ps, H, nq, plan):
+    ws = eph.Workspace(ps.ctx, nq, plan=plan)
+    out = eph.infer_batch(ps.ctx, ps.model, ws, H, nq)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint64).copy()
 
 
 @pytest.mark.parametrize("name,extra", [("c3", 77), ("c4", 123)])
@@ -65,19 +55,18 @@ def test_plan_variants_bit_identical(name, extra):
     Xs = np.ascontiguousarray(Xq[:nq])
     X = torch.from_numpy(Xs.view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)
-    ws = eph.Workspace(ps.ctx, nq)
-    ref = _run(ps, ws, H, nq, {})
+    ref = _run(ps, H, nq, None)
     om = opipe.build_model(cfg, P, Xtr, ytr)
     H_or = opipe.encode_queries(om, P, Xs)
     Sref = hdc.scores(H_or, om.class_hv)
     S, _ = eph.decrypt_scores(ps.ctx, ps.sk, ref, nq)
     assert np.array_equal(S, Sref)
-    for env in VARIANTS:
-        got = _run(ps, ws, H, nq, env)
-        assert np.array_equal(got, ref), env
+    for plan in VARIANTS:
+        got = _run(ps, H, nq, plan)
+        assert np.array_equal(got, ref), plan
 
 
-@pytest.mark.parametrize("name,groups", [("c3", "2"), ("c4", "7")])
+@pytest.mark.parametrize("name,groups", [("c3", 2), ("c4", 7)])
 def test_batch_groups_bit_identical(name, groups):
     """The FP64 path packs and evaluates the batches of a call in groups of at most
     m_batches (the plaintext workspace is capped at 32 GB; c4 beyond ~50 batches):
@@ -90,10 +79,6 @@ def test_batch_groups_bit_identical(name, groups):
     X = torch.from_numpy(np.ascontiguousarray(Xq[:nq]).view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)
     ref = eph.infer_batch(ps.ctx, ps.model, eph.Workspace(ps.ctx, nq), H, nq).cpu().numpy()
-    os.environ["EPHDC_M_BATCHES"] = groups
-    try:
-        ws = eph.Workspace(ps.ctx, nq)         # the knob is read when the workspace is made
-    finally:
-        os.environ.pop("EPHDC_M_BATCHES", None)
+    ws = eph.Workspace(ps.ctx, nq, plan={"m_batches": groups})
     got = eph.infer_batch(ps.ctx, ps.model, ws, H, nq).cpu().numpy()
     assert np.array_equal(got, ref)
