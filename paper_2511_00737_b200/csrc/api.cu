@@ -818,6 +818,7 @@ void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
         cudaFree(p->tw_f64);
         cudaFree(p->itw_f64);
         cudaFree(p->post_f64);
+        ephdc_ntt_plan_c5_free(p);
     }
     delete p;
 }
@@ -855,6 +856,11 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
     }
     plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
     if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
+    for (uint32_t j = 0; j < L; ++j) {
+        p->c5_w1[j] = tw[(size_t)j * N + 1].w;
+        p->c5_w1p[j] = tw[(size_t)j * N + 1].wp;
+    }
+
     if (p->fwd_f64 || p->inv_f64) {
         // FP64 tables: forward psi_rev; inverse = Cooley-Tukey DIT on the bit-reversed
         // input (x[r] = DFT(a psi^j)[brev r]): stage of half-size h uses omega^-(N/2h) jj
@@ -920,6 +926,10 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
         ephdc_ntt_plan_free(p.release());
         return EPHDC_ECUDA;
     }
+    if (p->fwd_f64 && plan_ntt_c5(p.get()) != cudaSuccess) {
+        ephdc_ntt_plan_free(p.release());
+        return EPHDC_ECUDA;
+    }
     *out = p.release();
     return EPHDC_OK;
 }
@@ -927,7 +937,8 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
 ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    const cudaError_t e = launch_ntt_batch_f64(p, d_polys, batch, false, (cudaStream_t)stream);
+    cudaError_t e = launch_ntt_c5(p, d_polys, batch, false, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) e = launch_ntt_batch_f64(p, d_polys, batch, false, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, false, (cudaStream_t)stream));
     else EPHDC_CUDA_TRY(e);
     return EPHDC_OK;
@@ -936,7 +947,8 @@ ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t 
 ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    const cudaError_t e = launch_ntt_batch_f64(p, d_polys, batch, true, (cudaStream_t)stream);
+    cudaError_t e = launch_ntt_c5(p, d_polys, batch, true, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) e = launch_ntt_batch_f64(p, d_polys, batch, true, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, true, (cudaStream_t)stream));
     else EPHDC_CUDA_TRY(e);
     return EPHDC_OK;

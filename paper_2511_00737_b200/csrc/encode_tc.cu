@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "internal.h"
+#include "tma_host.h"
 #include "tmem.cuh"
 
 namespace ephdc {
@@ -215,11 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) ephdc_tmem::dealloc(tmem_d, (uint32_t)kTileN);
 }
 
-// ---- host: tensor maps through the driver entry point (no -lcuda link) ----
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+}  // namespace
 
+// ---- host: tensor maps through the driver entry point (no -lcuda link; tma_host.h) ----
 EncodeTiledFn encode_tiled_fn() {
     static EncodeTiledFn fn = nullptr;
     static std::once_flag once;
@@ -232,6 +231,8 @@ EncodeTiledFn encode_tiled_fn() {
     });
     return fn;
 }
+
+namespace {
 
 // rows x F bytes, row-major; box 128 rows x 128 bytes, 128-byte swizzle, zero fill
 bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t F) {

@@ -132,6 +132,16 @@ struct ephdc_ntt_plan {
     // 0 = (q, 1/q); the inverse's scaling: GS N^-1 [L], DIT N^-1 psi^-j [L][N] (w, w/q)
     double2 *tw_f64 = nullptr, *itw_f64 = nullptr;
     double2 *post_f64 = nullptr;
+    // c5 kernels (ntt_c5.cu) when their bounds hold: level-0 twiddle psi_rev[1] with its
+    // Shoup companion, Barrett constants floor(2^64/q) and the offset K q of the final
+    // reduction, per prime
+    bool c5_fwd = false, c5_inv = false;
+    uint64_t c5_w1[EPHDC_MAX_PRIMES]{}, c5_w1p[EPHDC_MAX_PRIMES]{};
+    uint64_t c5_bm[EPHDC_MAX_PRIMES]{}, c5_off[EPHDC_MAX_PRIMES]{};
+    // inverse: DIT table [L][N] (W[h + jj] = omega^-(N/2h) jj, entry 0 = (q, 1/q)), fused
+    // last-level scaling [L][N/2][2] (s_j, s_j W[N/2 + j]), s_j = N^-1 psi^-j; c = psi^-N/2
+    double2 *c5_itw = nullptr, *c5_itail = nullptr;
+    double2 c5_cinv[EPHDC_MAX_PRIMES]{};
 };
 
 namespace ephdc {
@@ -195,6 +205,19 @@ struct StdF64Args {
 cudaError_t launch_ntt_batch_f64(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t batch, bool inverse,
                                  cudaStream_t st);
 void plan_ntt_f64(const std::vector<uint64_t> &q, uint32_t log2N, bool *fwd, bool *inv, bool *inv_dit);
+// c5 standalone kernels (ntt_c5.cu)
+struct C5Args {
+    u64 *polys;            // [batch][L][N], in place
+    const double2 *tw;     // forward: [L][N] (psi_rev[i], fl(psi_rev[i]/q_j)), entry 0 = (q_j, fl(1/q_j));
+                           // inverse: the DIT table ephdc_ntt_plan::c5_itw
+    const double2 *tail;   // inverse: ephdc_ntt_plan::c5_itail
+    u32 L, batch, items;   // items = L * batch (prime-major work order)
+    u64 q[kMaxL], w1[kMaxL], w1p[kMaxL], bm[kMaxL], off[kMaxL];
+    double2 cinv[kMaxL];   // inverse: psi^-N/2 as (w, w/q)
+};
+cudaError_t plan_ntt_c5(ephdc_ntt_plan *p);
+void ephdc_ntt_plan_c5_free(ephdc_ntt_plan *p);
+cudaError_t launch_ntt_c5(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t batch, bool inverse, cudaStream_t st);
 bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan);
 void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G);
 int ntt_mac_occupancy(uint32_t log2N, uint32_t S);

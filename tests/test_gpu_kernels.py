@@ -83,3 +83,25 @@ def test_ntt_c5_sampled_large_batch(log2N):
             assert np.array_equal(got[b, j], core.ntt_fwd(x[b, j][None, :], log2N, p, psi)[0]), (b, j)
     eph.ntt_inv(plan, d)
     assert np.array_equal(_host(d), x)
+
+
+@pytest.mark.parametrize("log2N,L,bits,batch", [(12, 16, 48, 300), (13, 16, 30, 97), (13, 5, 49, 1000),
+                                                (14, 9, 48, 77), (14, 3, 44, 400), (12, 1, 48, 1)])
+def test_ntt_c5_prime_switch(log2N, L, bits, batch):
+    """The persistent c5 kernels walk (prime, polynomial) items prime-major: per CTA the
+    range crosses prime boundaries (twiddles reloaded) and the TMA ring wraps many times;
+    every polynomial is checked against the oracle on a seeded sample."""
+    N = 1 << log2N
+    q = nt.prime_chain([bits] * L, log2N)
+    x = inp.gen_residues(q, batch, N, seed=9000 + log2N + L)
+    plan = eph.NttPlan(q, log2N)
+    d = _dev(x)
+    eph.ntt_fwd(plan, d)
+    got = _host(d)
+    rng = np.random.default_rng(batch)
+    for b in sorted({0, batch - 1, *rng.integers(0, batch, 5).tolist()}):
+        for j in sorted({0, L - 1, int(rng.integers(0, L))}):
+            psi = nt.min_primitive_2n_root(q[j], N)
+            assert np.array_equal(got[b, j], core.ntt_fwd(x[b, j][None, :], log2N, q[j], psi)[0]), (b, j)
+    eph.ntt_inv(plan, d)
+    assert np.array_equal(_host(d), x)
