@@ -54,7 +54,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: seconds of timed oracle steps (each step = one full batch)")
+    ap.add_argument("--threads", type=int, default=0, help="oracle threads (OMP_NUM_THREADS; 0 = all host cores)")
     ap.add_argument("--plan", default="", help="A/B only: workspace launch-plan overrides, e.g. 'flags=2,bg=8'")
     return ap.parse_args()
 
@@ -115,68 +117,87 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle
-def oracle_sample(cfg, data, budget_s: float):
-    """Oracle (plain CPU, OpenMP over dims) on a bounded sample of the workload:
-    encode + client evaluation of ONE full ciphertext batch (B queries) over the first
-    Ds dims with a stored model; queries/s extrapolated to all D_live dims."""
-    from oracle import pipeline as opipe
-    Xtr, ytr, Xq, P = data
-    om = opipe.build_model(cfg, P, Xtr, ytr)
-    bfv = om.bfv
-    B = bfv.B
-    Xb = Xq[:B]
-    cores = os.cpu_count() or 1
+class OracleSample:
+    """The oracle (plain CPU C + numpy, OpenMP over dims; TEST INFRASTRUCTURE, executed only
+    by this leg) on the unit of the workload: encode + client evaluation of ONE full
+    ciphertext batch (B queries) over ALL D_live dims against the stored model -- the
+    same arithmetic the GPU does per batch, nothing extrapolated.  The model is
+    encrypted once (untimed, like the resident GPU model)."""
 
-    def run(Ds):
-        C = np.ascontiguousarray(om.class_hv[:, :Ds])
-        bfv.D_live = Ds
-        model = bfv.encrypt_dims(C, om.enc_seed, 0, Ds)            # untimed: model is resident
+    def __init__(self, cfg, data):
+        from oracle import hdc, pipeline as opipe
+        Xtr, ytr, Xq, P = data
+        self.cfg, self.hdc, self.P = cfg, hdc, P
+        self.om = opipe.build_model(cfg, P, Xtr, ytr)
+        self.bfv = self.om.bfv
+        self.B = self.bfv.B
+        self.Xb = np.ascontiguousarray(Xq[: self.B])
+        self.model = self.bfv.encrypt_dims(self.om.class_hv, self.om.enc_seed, 0, cfg.D_live)
+
+    def step(self) -> float:
+        """One batch; returns its wall time in seconds."""
         t0 = time.perf_counter()
-        Pd = P[:Ds]
-        from oracle import hdc
-        H = hdc.quantise_queries(hdc.encode_raw(Pd, Xb, Ds), om.qshift, om.Qbits)
-        bfv.infer_batch(H, H.shape[1], 0, model=model)
-        dt = time.perf_counter() - t0
-        bfv.D_live = cfg.D_live
-        return dt
+        H = self.hdc.quantise_queries(self.hdc.encode_raw(self.P, self.Xb, self.cfg.D_live), self.om.qshift,
+                                      self.om.Qbits)
+        self.bfv.infer_batch(H, H.shape[1], 0, model=self.model)
+        return time.perf_counter() - t0
 
-    Ds = max(1, min(cfg.D_live, 2 * cores))
-    dt = run(Ds)
-    if dt < budget_s / 3:
-        Ds = int(min(cfg.D_live, max(Ds + 1, Ds * budget_s / max(dt, 1e-3))))
-        dt = run(Ds)
-    per_batch = dt * cfg.D_live / Ds
-    qps = B / per_batch
-    return {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle",
-            "sample": f"{cfg.name}: encode + evaluation of one full batch ({B} queries) over {Ds} of "
-                      f"{cfg.D_live} dims with a stored model, {dt:.1f} s, extrapolated linearly in D"}
+    def describe(self, dt: float, threads: int) -> str:
+        return (f"{self.cfg.name}: encode + evaluation of one full batch ({self.B} queries, all "
+                f"{self.cfg.D_live} dims x {self.bfv.L} primes, model resident) in {dt:.1f} s on {threads} "
+                f"thread(s); batches are identical units (one scores ciphertext each), no extrapolation")
+
+
+def oracle_threads() -> int:
+    return int(os.environ.get("OMP_NUM_THREADS") or os.cpu_count() or 1)
+
+
+def cpu_baseline(cfg, data) -> dict:
+    o = OracleSample(cfg, data)
+    dt = o.step()
+    return {"value": o.B / dt, "unit": "queries/s", "cores": oracle_threads(), "kind": "oracle",
+            "sample": o.describe(dt, oracle_threads())}
 
 
 # ----------------------------------------------------------------------------- main
 def main():
     a = parse()
+    if a.threads > 0:   # before the oracle's OpenMP runtime loads
+        os.environ["OMP_NUM_THREADS"] = str(a.threads)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = inp.CONFIGS[a.config]
 
     if a.impl == "reference":
+        # the oracle as it stands on the host cores (rank 0 only); a step = one full batch.
+        # Steps are capped so the run ends within --ref-budget seconds; the line reports the
+        # steps it actually timed.
         if rank != 0:
             return 0
         Xtr, ytr, Xq, _ = inp.gen_features(cfg)
         P = inp.gen_projection(cfg)
-        vals = []
-        cb = None
-        for _ in range(a.warmup + a.steps):
-            cb = oracle_sample(cfg, (Xtr, ytr, Xq, P), a.cpu_budget / max(1, a.steps))
-            vals.append(cb["value"])
-        v = statistics.median(vals[a.warmup:])
-        cb["value"] = v
+        o = OracleSample(cfg, (Xtr, ytr, Xq, P))
+        t_first = o.step()                                        # warm-up step 1
+        budget = max(a.ref_budget, 2 * t_first)
+        warm = 1
+        while warm < a.warmup and (warm + 1) * t_first < 0.25 * budget:
+            o.step()
+            warm += 1
+        steps = max(1, min(a.steps, int((budget - warm * t_first) // max(t_first, 1e-3))))
+        times = [o.step() for _ in range(steps)]
+        ms = 1e3 * sum(times) / steps
+        v = o.B / (ms / 1e3)
+        threads = oracle_threads()
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": a.gpus,
-                "steps": a.steps, "warmup": a.warmup, "ms_per_step": cfg.nq / v * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-                "config": {"workload": cfg.name, "nq": cfg.nq, "N": cfg.N, "L": cfg.L, "D": cfg.D_live, "k": cfg.k},
-                "cpu_baseline": cb,
+                "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u64 (exact modular integers, CPU)",
+                "data": "synthetic",
+                "config": {"workload": cfg.name, "queries_per_step": o.B, "N": cfg.N, "L": cfg.L, "D": cfg.D_live,
+                           "k": cfg.k, "requested": {"steps": a.steps, "warmup": a.warmup},
+                           "threads": threads},
+                "cpu_baseline": {"value": v, "unit": "queries/s", "cores": threads, "kind": "oracle",
+                                 "sample": o.describe(ms / 1e3, threads)},
                 "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return 0
@@ -279,6 +300,18 @@ def main():
                 "share_of_step": round(mac_ms / max(total_ms, 1e-9), 4),
                 "kernel_ms": {k: round(v[0] / a.steps, 3) for k, v in kt.items()}}
 
+    # pipe / DRAM figures of the step's kernels from the committed ncu capture of this
+    # config (profiles/ncu_metrics.json, written by tools/ncu_metrics.py from an
+    # `ncu --set full` run of this bench command; ncu figures, not this run's)
+    ncu = None
+    try:
+        nm = json.load(open(os.path.join(ROOT, "profiles", "ncu_metrics.json"))).get(cfg.name)
+        if nm:
+            ncu = dict(nm)
+            ncu["hbm_peak_gbs"] = measured_peaks().get("hbm_gbs")
+    except Exception:
+        pass
+
     # e2e: the same step through the host-buffer C-ABI call (H2D + compute + D2H per step)
     e2e = None
     if not a.no_e2e:
@@ -305,18 +338,20 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = oracle_sample(cfg, (Xtr, ytr, Xq, P), a.cpu_budget)
+        cpu = cpu_baseline(cfg, (Xtr, ytr, Xq, P))
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64" if ctx.arith == "f64" else "u64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": ("u64 residues, exact modular arithmetic on the FP64 pipe" if ctx.arith == "f64"
+                          else "u64 residues, integer pipe"), "data": "synthetic",
                 "config": {"workload": cfg.name, "nq_per_gpu": nq, "batches": nb, "N": N, "L": L, "D": D,
                            "k": cfg.k, "F": cfg.F, "t": ctx.t, "log2q": sum(int(q).bit_length() for q in ctx.q),
                            "parallelism": f"replica x{world} (independent query batches)",
                            "arith": ctx.arith,
                            "l2": "inputs larger than L2 (encrypted model %.1f GB in HBM)" % (D * L * 2 * N * 8 / 1e9)},
-                "gpu_launches": int(launches), "clocks": clk, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e}
+                "gpu_launches": int(launches), "clocks": clk, "roofline": roofline, "ncu": ncu, "cpu_baseline": cpu,
+                "e2e": e2e}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

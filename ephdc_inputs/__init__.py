@@ -140,3 +140,38 @@ def c5_max_batch(log2N: int, L: int, word_bytes: int = 8) -> int:
     N = 1 << log2N
     per_term = 3 * L * N * word_bytes          # 2 ciphertext polys + 1 plaintext poly
     return max(1, (C5_WORKING_SET_CAP - 2 * L * N * word_bytes) // per_term)
+
+
+# c5 sweep (BASELINE.json configs[4]): word classes -- 30-bit primes (u64 words; u32
+# words through the *32 entry points), 48-bit (the FP64 kernels' range) and 60-bit
+# primes -- for every N and L; batches 1 ... 65536 capped by the 32 GB working set.
+C5_PRIME_BITS = (30, 48, 60)
+
+
+def c5_points(kind: str = "all"):
+    """[(log2N, L, bits, word_bytes, [batches])] of the c5 sweep.  kind: "all" (every
+    N x L x word class, batches C5_BATCHES capped at the working set) or "quick"."""
+    pts = []
+    if kind == "quick":
+        grid = [(lg, L, b, 8) for lg in C5_LOG2N for L, b in ((9, 48), (5, 60), (16, 30))]
+    else:
+        grid = [(lg, L, b, 8) for lg in C5_LOG2N for L in C5_L for b in C5_PRIME_BITS]
+        grid += [(lg, L, 30, 4) for lg in C5_LOG2N for L in C5_L]
+    for lg, L, b, wb in grid:
+        cap = max(1, C5_WORKING_SET_CAP // (L * (1 << lg) * wb))
+        bs = sorted({min(x, cap) for x in C5_BATCHES})
+        pts.append((lg, L, b, wb, bs))
+    return pts
+
+
+def c5_residues_torch(moduli: List[int], n_poly: int, N: int, seed: int, device, dtype=None):
+    """Uniform residues [n_poly, L, N] (int64, or the given torch dtype) generated ON the
+    device with torch's seeded Philox generator: the bulk inputs of the c5 sweep (too
+    large for numpy); tests copy the sampled polynomials they check back to the host."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    out = torch.empty((n_poly, len(moduli), N), dtype=torch.int64, device=device)
+    for j, q in enumerate(moduli):
+        out[:, j, :] = torch.randint(0, int(q), (n_poly, N), generator=g, device=device, dtype=torch.int64)
+    return out if dtype is None else out.to(dtype)

@@ -142,6 +142,25 @@ ephdc_status ephdc_min_psi(uint64_t p, uint32_t log2N, uint64_t *psi);
 /* CDT thresholds of the discrete Gaussian sampler (reading #10): out[20]. */
 ephdc_status ephdc_gaussian_cdt(double sigma, uint64_t *out20);
 
+/* Query hypervector width (reading #12; the paper's Q bits): the largest
+ * Q <= 8 with D_live * (2^(Q-1) - 1) * (2^(Cbits-1) - 1) <= (t-1)/2, so that no score
+ * wraps mod t.  EPARAM if even Q = 2 wraps or Cbits is outside 2..8. */
+ephdc_status ephdc_query_bits(uint32_t D_live, uint32_t Cbits, uint64_t t, uint32_t *Qbits);
+
+/* Server model build (CS1; once, untimed): single-pass training and quantisation.
+ * h_acc [D_live][n] int32: the raw projections of the n training samples
+ * (ephdc_encode_raw); h_labels [n] in 0..k-1.
+ *   class sums   v_c[d] = sum_{i: label i = c} acc[d][i]
+ *   class HVs    C_c[d] = sign(v) floor((2|v| cmax + M_c) / (2 M_c)), M_c = max_d |v_c[d]|,
+ *                cmax = 2^(Cbits-1) - 1 (round half away from zero, reading #14)
+ *   query shift  *qshift = the smallest s >= 0 with max|acc| <= qmax 2^s, qmax =
+ *                2^(Qbits-1) - 1 (max-abs calibration, reading #13)
+ * h_class_hv [k][D_live] int8.  Host-only (no device needed).  Errors: ENULL, EPARAM
+ * (k = 0, a label >= k, Cbits / Qbits outside 2..8). */
+ephdc_status ephdc_train_model(uint32_t D_live, uint32_t n, uint32_t k, uint32_t Cbits, uint32_t Qbits,
+                               const int32_t *h_acc, const int64_t *h_labels, int8_t *h_class_hv,
+                               uint32_t *qshift);
+
 /* Number of CUDA kernels this library has launched in this process (all
  * entry points).  Used by bench.py for the gpu_launches claim. */
 uint64_t ephdc_launch_count(void);
@@ -347,6 +366,25 @@ ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t 
  * Async (the call zeroes d_out itself). */
 ephdc_status ephdc_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
                        uint64_t *d_out, void *stream);
+
+/* The same three operations on 32-bit words (30-bit primes in u32): every
+ * array is uint32 with the layouts above; the plan's primes must all be < 2^30
+ * (EPARAM otherwise).  Integer-pipe u32 Shoup butterflies; MAC products accumulate
+ * exactly in 64 bits.  Async. */
+ephdc_status ephdc_ntt_fwd32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, void *stream);
+ephdc_status ephdc_ntt_inv32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, void *stream);
+ephdc_status ephdc_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,
+                         uint32_t *d_out, void *stream);
+
+/* Which kernels a plan runs (tests and the microbench report). */
+#define EPHDC_NTT_KERNEL_INT 0u     /* integer pipe, u64 Shoup (any prime < 2^61)          */
+#define EPHDC_NTT_KERNEL_F64 1u     /* FP64 pipe, per-polynomial CTAs (round-1 kernels)    */
+#define EPHDC_NTT_KERNEL_C5_F64 2u  /* FP64 pipe, persistent TMA-fed kernels (ntt_c5.cu)   */
+typedef struct {
+    uint32_t fwd_kernel, inv_kernel;  /* EPHDC_NTT_KERNEL_*                               */
+    uint32_t u32_words;               /* 1 if the *32 entry points are available          */
+} ephdc_ntt_plan_info;
+ephdc_status ephdc_ntt_plan_query(const ephdc_ntt_plan *p, ephdc_ntt_plan_info *info);
 
 #ifdef __cplusplus
 }

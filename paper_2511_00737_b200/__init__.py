@@ -18,11 +18,11 @@ from ._capi import EphdcError, call, lib
 
 __all__ = [
     "Context", "SecretKey", "EncryptedModel", "Workspace", "NttPlan", "EphdcError",
-    "find_ntt_primes", "min_psi", "gaussian_cdt", "launch_count",
+    "find_ntt_primes", "min_psi", "gaussian_cdt", "query_bits", "train_model", "launch_count",
     "encode_queries", "encode_raw", "infer_batch", "encode_plaintexts", "classify_host",
     "scores_message_bytes", "pack_scores", "unpack_scores", "classify_host_packed",
     "sr_encrypt_queries", "sr_model_plaintexts", "sr_evaluate",
-    "decrypt_scores", "decrypt_slots", "ntt_fwd", "ntt_inv", "mac",
+    "decrypt_scores", "decrypt_slots", "ntt_fwd", "ntt_inv", "mac", "ntt_fwd32", "ntt_inv32", "mac32",
 ]
 
 
@@ -61,6 +61,25 @@ def min_psi(p: int, log2N: int) -> int:
     out = ctypes.c_uint64()
     call("ephdc_min_psi", p, log2N, ctypes.addressof(out))
     return int(out.value)
+
+
+def query_bits(D_live: int, Cbits: int, t: int) -> int:
+    """ephdc_query_bits: reading #12."""
+    out = ctypes.c_uint32()
+    call("ephdc_query_bits", D_live, Cbits, t, ctypes.addressof(out))
+    return int(out.value)
+
+
+def train_model(acc_train: np.ndarray, y_train: np.ndarray, k: int, Cbits: int, Qbits: int) -> Tuple[np.ndarray, int]:
+    """ephdc_train_model: bundle + quantise the class HVs, calibrate the query shift.
+    acc_train int32 [D_live][n]; returns (class_hv int8 [k][D_live], qshift)."""
+    acc = np.ascontiguousarray(acc_train, dtype=np.int32)
+    lab = np.ascontiguousarray(y_train, dtype=np.int64)
+    D, n = acc.shape
+    C = np.zeros((k, D), dtype=np.int8)
+    s = ctypes.c_uint32()
+    call("ephdc_train_model", D, n, k, Cbits, Qbits, _np_ptr(acc), _np_ptr(lab), _np_ptr(C), ctypes.addressof(s))
+    return C, int(s.value)
 
 
 def gaussian_cdt(sigma: float = 3.2) -> np.ndarray:
@@ -373,6 +392,11 @@ class NttPlan:
         self._h = ctypes.c_void_p()
         call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device, 1 if force_int else 0,
              ctypes.byref(self._h))
+        info = (ctypes.c_uint32 * 3)()
+        call("ephdc_ntt_plan_query", self._h, ctypes.addressof(info))
+        names = {0: "int", 1: "f64", 2: "c5_f64"}
+        self.fwd_kernel, self.inv_kernel = names[info[0]], names[info[1]]
+        self.u32_words = bool(info[2])
 
     @property
     def handle(self):
@@ -394,6 +418,26 @@ def ntt_fwd(plan: NttPlan, polys, stream=None):
 def ntt_inv(plan: NttPlan, polys, stream=None):
     call("ephdc_ntt_inv", plan.handle, _dptr(polys), polys.numel() // (plan.L * plan.N), _stream(stream))
     return polys
+
+
+def ntt_fwd32(plan: NttPlan, polys, stream=None):
+    """u32 words (torch.int32 storage of residues < 2^30)."""
+    call("ephdc_ntt_fwd32", plan.handle, _dptr(polys), polys.numel() // (plan.L * plan.N), _stream(stream))
+    return polys
+
+
+def ntt_inv32(plan: NttPlan, polys, stream=None):
+    call("ephdc_ntt_inv32", plan.handle, _dptr(polys), polys.numel() // (plan.L * plan.N), _stream(stream))
+    return polys
+
+
+def mac32(plan: NttPlan, ct, pt, out=None, stream=None):
+    import torch
+    D = pt.shape[0]
+    if out is None:
+        out = torch.empty((plan.L, 2, plan.N), dtype=torch.int32, device=pt.device)
+    call("ephdc_mac32", plan.handle, _dptr(ct), _dptr(pt), D, _dptr(out), _stream(stream))
+    return out
 
 
 def mac(plan: NttPlan, ct, pt, out=None, stream=None):

@@ -60,6 +60,8 @@ _SIGS = {
     "ephdc_min_psi": (c_st, [c_u64, c_u32, c_vp]),
     "ephdc_gaussian_cdt": (c_st, [ctypes.c_double, c_vp]),
     "ephdc_launch_count": (c_u64, []),
+    "ephdc_query_bits": (c_st, [c_u32, c_u32, c_u64, c_vp]),
+    "ephdc_train_model": (c_st, [c_u32, c_u32, c_u32, c_u32, c_u32, c_vp, c_vp, c_vp, c_vp]),
     "ephdc_ctx_create": (c_st, [ctypes.POINTER(Params), c_int, c_vp]),
     "ephdc_ctx_free": (None, [c_vp]),
     "ephdc_ctx_query": (c_st, [c_vp, ctypes.POINTER(CtxInfo)]),
@@ -94,6 +96,10 @@ _SIGS = {
     "ephdc_ntt_fwd": (c_st, [c_vp, c_vp, c_u32, c_vp]),
     "ephdc_ntt_inv": (c_st, [c_vp, c_vp, c_u32, c_vp]),
     "ephdc_mac": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
+    "ephdc_ntt_fwd32": (c_st, [c_vp, c_vp, c_u32, c_vp]),
+    "ephdc_ntt_inv32": (c_st, [c_vp, c_vp, c_u32, c_vp]),
+    "ephdc_mac32": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
+    "ephdc_ntt_plan_query": (c_st, [c_vp, c_vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -112,6 +112,51 @@ const char *ephdc_status_string(ephdc_status s) {
 
 int ephdc_abi_version(void) { return EPHDC_ABI_VERSION; }
 
+ephdc_status ephdc_query_bits(uint32_t D_live, uint32_t Cbits, uint64_t t, uint32_t *Qbits) {
+    if (!Qbits) return EPHDC_ENULL;
+    if (Cbits < 2 || Cbits > 8 || t < 3) return EPHDC_EPARAM;
+    const uint64_t cmax = (1u << (Cbits - 1)) - 1, limit = (t - 1) / 2;
+    for (uint32_t Q = 8; Q >= 2; --Q)
+        if ((uint64_t)D_live * ((1u << (Q - 1)) - 1) * cmax <= limit) {
+            *Qbits = Q;
+            return EPHDC_OK;
+        }
+    return EPHDC_EPARAM;
+}
+
+ephdc_status ephdc_train_model(uint32_t D_live, uint32_t n, uint32_t k, uint32_t Cbits, uint32_t Qbits,
+                               const int32_t *h_acc, const int64_t *h_labels, int8_t *h_class_hv,
+                               uint32_t *qshift) {
+    if (!h_class_hv || !qshift || ((!h_acc || !h_labels) && n && D_live)) return EPHDC_ENULL;
+    if (k == 0 || Cbits < 2 || Cbits > 8 || Qbits < 2 || Qbits > 8) return EPHDC_EPARAM;
+    for (uint32_t i = 0; i < n; ++i)
+        if (h_labels[i] < 0 || (uint64_t)h_labels[i] >= k) return EPHDC_EPARAM;
+    const int64_t cmax = (1 << (Cbits - 1)) - 1, qmax = (1 << (Qbits - 1)) - 1;
+    std::vector<int64_t> v((size_t)k * D_live, 0);
+    int64_t peak = 0;
+    for (uint32_t d = 0; d < D_live; ++d) {
+        const int32_t *row = h_acc + (size_t)d * n;
+        for (uint32_t i = 0; i < n; ++i) {
+            v[(size_t)h_labels[i] * D_live + d] += row[i];
+            peak = std::max<int64_t>(peak, row[i] < 0 ? -(int64_t)row[i] : row[i]);
+        }
+    }
+    for (uint32_t c = 0; c < k; ++c) {
+        const int64_t *vc = v.data() + (size_t)c * D_live;
+        int64_t M = 0;
+        for (uint32_t d = 0; d < D_live; ++d) M = std::max<int64_t>(M, vc[d] < 0 ? -vc[d] : vc[d]);
+        for (uint32_t d = 0; d < D_live; ++d) {
+            const int64_t a = vc[d] < 0 ? -vc[d] : vc[d];
+            const int64_t r = M == 0 ? 0 : (2 * a * cmax + M) / (2 * M);
+            h_class_hv[(size_t)c * D_live + d] = (int8_t)(vc[d] < 0 ? -r : r);
+        }
+    }
+    uint32_t s = 0;
+    while ((qmax << s) < peak) ++s;
+    *qshift = s;
+    return EPHDC_OK;
+}
+
 uint64_t ephdc_launch_count(void) { return g_launches.load(); }
 
 ephdc_status ephdc_find_ntt_primes(uint32_t log2N, const uint32_t *bits, uint32_t count, const uint64_t *exclude,
@@ -818,6 +863,9 @@ void ephdc_ntt_plan_free(ephdc_ntt_plan *p) {
         cudaFree(p->tw_f64);
         cudaFree(p->itw_f64);
         cudaFree(p->post_f64);
+        cudaFree(p->tw32);
+        cudaFree(p->itw32);
+        cudaFree(p->ninv32);
         ephdc_ntt_plan_c5_free(p);
     }
     delete p;
@@ -926,6 +974,31 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
         ephdc_ntt_plan_free(p.release());
         return EPHDC_ECUDA;
     }
+    // u32 words when every prime < 2^30 (lazy [0, 4q) fits 32 bits)
+    if (*std::max_element(p->q.begin(), p->q.end()) < (1ull << 30)) {
+        std::vector<TwPair<u32>> t32((size_t)L * N), it32((size_t)L * N);
+        std::vector<uint32_t> n32(2 * L);
+        for (size_t i = 0; i < t32.size(); ++i) {
+            const uint32_t qj = (uint32_t)q[i / N];
+            t32[i] = TwPair<u32>{(u32)tw[i].w, shoup32((u32)tw[i].w, qj)};
+            it32[i] = TwPair<u32>{(u32)itw[i].w, shoup32((u32)itw[i].w, qj)};
+        }
+        for (uint32_t j = 0; j < L; ++j) {
+            n32[2 * j] = (uint32_t)ninv[2 * j];
+            n32[2 * j + 1] = shoup32(n32[2 * j], (uint32_t)q[j]);
+        }
+        if (dev_alloc(&p->tw32, t32.size()) != cudaSuccess || dev_alloc(&p->itw32, it32.size()) != cudaSuccess ||
+            dev_alloc(&p->ninv32, n32.size()) != cudaSuccess) {
+            ephdc_ntt_plan_free(p.release());
+            return EPHDC_ERESOURCE;
+        }
+        if (cudaMemcpy(p->tw32, t32.data(), sizeof(t32[0]) * t32.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(p->itw32, it32.data(), sizeof(it32[0]) * it32.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(p->ninv32, n32.data(), sizeof(uint32_t) * n32.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            ephdc_ntt_plan_free(p.release());
+            return EPHDC_ECUDA;
+        }
+    }
     if (p->fwd_f64 && plan_ntt_c5(p.get()) != cudaSuccess) {
         ephdc_ntt_plan_free(p.release());
         return EPHDC_ECUDA;
@@ -951,6 +1024,39 @@ ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t 
     if (e == cudaErrorNotSupported) e = launch_ntt_batch_f64(p, d_polys, batch, true, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, true, (cudaStream_t)stream));
     else EPHDC_CUDA_TRY(e);
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_ntt_fwd32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, void *stream) {
+    if (!p || (!d_polys && batch)) return EPHDC_ENULL;
+    if (!p->tw32) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(p->device));
+    EPHDC_CUDA_TRY(launch_ntt_batch32(p, d_polys, batch, false, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_ntt_inv32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, void *stream) {
+    if (!p || (!d_polys && batch)) return EPHDC_ENULL;
+    if (!p->tw32) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(p->device));
+    EPHDC_CUDA_TRY(launch_ntt_batch32(p, d_polys, batch, true, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,
+                         uint32_t *d_out, void *stream) {
+    if (!p || !d_out || ((!d_ct || !d_pt) && D)) return EPHDC_ENULL;
+    if (!p->tw32) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(p->device));
+    EPHDC_CUDA_TRY(launch_mac32(p, d_ct, d_pt, D, d_out, (cudaStream_t)stream));
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_ntt_plan_query(const ephdc_ntt_plan *p, ephdc_ntt_plan_info *info) {
+    if (!p || !info) return EPHDC_ENULL;
+    info->fwd_kernel = p->c5_fwd ? EPHDC_NTT_KERNEL_C5_F64 : p->fwd_f64 ? EPHDC_NTT_KERNEL_F64 : EPHDC_NTT_KERNEL_INT;
+    info->inv_kernel = p->c5_inv ? EPHDC_NTT_KERNEL_C5_F64 : p->inv_f64 ? EPHDC_NTT_KERNEL_F64 : EPHDC_NTT_KERNEL_INT;
+    info->u32_words = p->tw32 != nullptr;
     return EPHDC_OK;
 }
 

@@ -124,6 +124,9 @@ struct ephdc_ntt_plan {
     ephdc::PrimeSet ps{};
     TwPair<u64> *tw = nullptr, *itw = nullptr;  // [L][N]
     uint64_t *ninv = nullptr;                            // [L][2] (N^-1, Shoup)
+    // u32 words (every q_j < 2^30; ephdc_ntt_*32): the same tables in 32 bits
+    TwPair<u32> *tw32 = nullptr, *itw32 = nullptr;  // [L][N]
+    uint32_t *ninv32 = nullptr;                      // [L][2]
     // FP64 path (kernels_f64.cu k_ntt_std_f64) when the bounds allow it
     bool fwd_f64 = false, inv_f64 = false;
     bool inv_dit = false;   // FP64 inverse form: Cooley-Tukey DIT (true) or Gentleman-Sande
@@ -173,6 +176,10 @@ cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_
                              cudaStream_t st);
 cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
                        uint64_t *d_out, cudaStream_t st);
+cudaError_t launch_ntt_batch32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, bool inverse,
+                               cudaStream_t st);
+cudaError_t launch_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,
+                         uint32_t *d_out, cudaStream_t st);
 size_t ntt_mac_smem_bytes(uint32_t log2Nc);
 // tcgen05 int8 encoder (encode_tc.cu)
 bool encode_tc_supported(const ephdc_ctx *c);

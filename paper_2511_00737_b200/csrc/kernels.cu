@@ -24,6 +24,9 @@ std::atomic<uint64_t> g_launches{0};
 using namespace ephdc_ntt;
 
 constexpr int kE = 16;  // elements per thread in every NTT pass
+// one CTA per 2^14-coefficient polynomial: 32 elements per thread (512 threads keep 128
+// registers each; 1024 threads x 64 registers spilled)
+template <int LG> constexpr int batch_E() { return LG >= 14 ? 32 : kE; }
 
 // streaming (evict-first) 64-bit load for data read once
 EPHDC_D u64 ldcs64(const u64 *p) { return (u64)__ldcs(reinterpret_cast<const unsigned long long *>(p)); }
@@ -332,9 +335,10 @@ __global__ void k_finalize(u64 *__restrict__ out, u32 L, u32 N, PrimeSet ps, u32
 
 // Plaintext NTTs for parity export: p_hat[dd][j] = NTT_j(lift(M[dd])) (full N, one CTA per (dd, j)).
 template <int LG>
-__global__ void __launch_bounds__((1 << LG) / kE)
+__global__ void __launch_bounds__((1 << LG) / batch_E<LG>())
     k_plaintext_ntt(const u32 *__restrict__ M, u64 *__restrict__ pt, MacArgs a) {
-    constexpr int N = 1 << LG, NT = N / kE;
+    constexpr int E = batch_E<LG>();
+    constexpr int N = 1 << LG, NT = N / E;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
     const u32 j = blockIdx.x % a.L, dd = blockIdx.x / a.L;
@@ -344,10 +348,10 @@ __global__ void __launch_bounds__((1 << LG) / kE)
         const u32 v = m[pos];
         return (int)v >= 0 ? (u64)v : (u64)(int64_t)(int)v + q;
     };
-    fwd_ntt<u64, LG, kE>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
+    fwd_ntt<u64, LG, E>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
     u64 *o = pt + ((size_t)dd * a.L + j) * N;
 #pragma unroll
-    for (int e = 0; e < kE; ++e) {
+    for (int e = 0; e < E; ++e) {
         const int pos = threadIdx.x + e * NT;
         o[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
     }
@@ -366,9 +370,10 @@ struct EncArgs {
 };
 
 template <int LG>
-__global__ void __launch_bounds__((1 << LG) / kE)
+__global__ void __launch_bounds__((1 << LG) / batch_E<LG>())
     k_encrypt(const u32 *__restrict__ M, u64 g0, EncArgs a, u64 *__restrict__ out) {
-    constexpr int N = 1 << LG, NT = N / kE;
+    constexpr int E = batch_E<LG>();
+    constexpr int N = 1 << LG, NT = N / E;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     u64 *buf = reinterpret_cast<u64 *>(smem_raw);
     __shared__ u64 cdt[ephdc_rng::kCdtLen];
@@ -384,13 +389,13 @@ __global__ void __launch_bounds__((1 << LG) / kE)
         const int e = ephdc_rng::gaussian(seed, d, (u32)pos, cdt);
         return e >= 0 ? x + (u64)e : x + q - (u64)(-e);                     // [0, 4q)
     };
-    fwd_ntt<u64, LG, kE>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
+    fwd_ntt<u64, LG, E>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
     u64 *c0 = out + (((size_t)dd * a.L + j) * 2) * N;
     u64 *c1 = c0 + N;
     const u64 *sh = a.shat_mont + (size_t)j * N;
     const u64 mask = a.ps.mask[j];
 #pragma unroll 4
-    for (int e = 0; e < kE; ++e) {
+    for (int e = 0; e < E; ++e) {
         const int pos = threadIdx.x + e * NT;
         const u64 xh = reduce4<u64>(buf[pad(pos)], q, 2 * q);
         const u64 av = ephdc_rng::uniform_mod(seed, d, j, a.L, (u32)pos, q, mask);
@@ -407,36 +412,46 @@ __global__ void __launch_bounds__((1 << LG) / kE)
 // group per thread, straight from/to HBM) and S = N / 2^14 CTAs each transform one
 // slice of 2^14 coefficients in shared memory.
 // =====================================================================================
-struct NttArgs {
+// Word type W: u64 residues (any prime < 2^61) or u32 residues (primes < 2^30: the lazy
+// [0, 4q) range fits 32 bits) -- the c5 sweep's two word classes.
+template <typename W> struct NttArgsW {
     PrimeSet ps;
     u32 L;
     u32 log2N;               // full transform size (slices: LG < log2N)
-    const TwPair<u64> *tw;   // [L][N]
-    const u64 *ninv;         // [L][2]
+    const TwPair<W> *tw;     // [L][N]
+    const W *ninv;           // [L][2]
 };
+using NttArgs = NttArgsW<u64>;
+
+template <typename W> EPHDC_D W ld_stream(const W *p) {
+    if constexpr (sizeof(W) == 8) return (W)__ldcs(reinterpret_cast<const unsigned long long *>(p));
+    else return (W)__ldcs(reinterpret_cast<const unsigned int *>(p));
+}
+template <typename W> EPHDC_D void st_stream(W *p, W v) {
+    if constexpr (sizeof(W) == 8) __stcs(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);
+    else __stcs(reinterpret_cast<unsigned int *>(p), (unsigned int)v);
+}
 
 // elements per thread: 16, or 32 at 2^14 points (512 threads x 128 registers: no spills)
-template <int LG> constexpr int batch_E() { return LG >= 14 ? 32 : kE; }
-
-template <int LG, bool INV>
-__global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(u64 *__restrict__ polys, NttArgs a) {
+template <int LG, bool INV, typename W = u64>
+__global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(W *__restrict__ polys, NttArgsW<W> a) {
     constexpr int E = batch_E<LG>();
     constexpr int NC = 1 << LG, NT = NC / E;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    u64 *buf = reinterpret_cast<u64 *>(smem_raw);
+    W *buf = reinterpret_cast<W *>(smem_raw);
     const u32 S = 1u << (a.log2N - LG), N = 1u << a.log2N;
     const u32 s = blockIdx.x % S, pj = blockIdx.x / S;   // pj = poly * L + j
     const u32 j = pj % a.L;
-    u64 *p = polys + (size_t)pj * N + (size_t)s * NC;
-    const u64 q = a.ps.q[j];
-    const TwPair<u64> *tw = a.tw + (size_t)j * N;
-    auto load = [&](int pos) -> u64 { return p[pos]; };
+    W *p = polys + (size_t)pj * N + (size_t)s * NC;
+    const W q = (W)a.ps.q[j];
+    const TwPair<W> *tw = a.tw + (size_t)j * N;
+    auto load = [&](int pos) -> W { return p[pos]; };
     if constexpr (!INV) {
-        fwd_ntt<u64, LG, E>(buf, load, tw, N + s * NC, q);
+        fwd_ntt<W, LG, E>(buf, load, tw, N + s * NC, q);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int pos = threadIdx.x + e * NT;
-            p[pos] = reduce4<u64>(buf[pad(pos)], q, 2 * q);
+            p[pos] = reduce4<W>(buf[sidx<W>(pos)], q, (W)(2 * q));
         }
     } else {
         // the first inverse pass groups E consecutive residues per thread: stage the
@@ -446,23 +461,23 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(u64 *__
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int pos = threadIdx.x + e * NT;
-            buf[pad(pos)] = p[pos];
+            buf[sidx<W>(pos)] = p[pos];
         }
         __syncthreads();
-        auto sload = [&](int pos) -> u64 { return buf[pad(pos)]; };
-        inv_ntt<u64, LG, E>(buf, sload, tw, q, N + s * NC);
+        auto sload = [&](int pos) -> W { return buf[sidx<W>(pos)]; };
+        inv_ntt<W, LG, E>(buf, sload, tw, q, N + s * NC);
         if (S == 1) {
-            const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
+            const W ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int pos = threadIdx.x + e * NT;
-                p[pos] = csub(mul_shoup_lazy<u64>(buf[pad(pos)], ni, nip, q), q);
+                p[pos] = csub(mul_shoup_lazy<W>(buf[sidx<W>(pos)], ni, nip, q), q);
             }
         } else {  // lazy [0, 2q): the global stages and N^-1 follow in k_ntt_global
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int pos = threadIdx.x + e * NT;
-                p[pos] = buf[pad(pos)];
+                p[pos] = buf[sidx<W>(pos)];
             }
         }
     }
@@ -471,48 +486,90 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(u64 *__
 // The GS = log2(N) - 14 global stages: forward (CT; first stages, canonical input ->
 // lazy [0, 4q)) or inverse (GS; last stages, lazy [0, 2q) input -> times N^-1,
 // canonical).  Thread = one radix-2^GS group {i + k * N/2^GS}.
-template <int GS, bool INV>
-__global__ void __launch_bounds__(256) k_ntt_global(u64 *__restrict__ polys, u32 n_polys, NttArgs a) {
+template <int GS, bool INV, typename W = u64>
+__global__ void __launch_bounds__(256) k_ntt_global(W *__restrict__ polys, u32 n_polys, NttArgsW<W> a) {
     constexpr int R = 1 << GS;
     const u32 N = 1u << a.log2N, T = N >> GS;
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (size_t)n_polys * T) return;
     const u32 pj = (u32)(gid / T), i = (u32)(gid % T), j = pj % a.L;
-    u64 *p = polys + (size_t)pj * N + i;
-    const u64 q = a.ps.q[j], two_q = 2 * q;
-    const TwPair<u64> *tw = a.tw + (size_t)j * N;
-    u64 x[R];
+    W *p = polys + (size_t)pj * N + i;
+    const W q = (W)a.ps.q[j], two_q = (W)(2 * q);
+    const TwPair<W> *tw = a.tw + (size_t)j * N;
+    W x[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) x[k] = __ldcs(reinterpret_cast<const unsigned long long *>(p + (size_t)k * T));
+    for (int k = 0; k < R; ++k) x[k] = ld_stream<W>(p + (size_t)k * T);
     if constexpr (!INV) {
 #pragma unroll
         for (int sub = 0; sub < GS; ++sub) {
             const int h = R >> (sub + 1);
 #pragma unroll
             for (int v = 0; v < (1 << sub); ++v) {
-                const TwPair<u64> w = tw[(1 << sub) + v];
+                const TwPair<W> w = tw[(1 << sub) + v];
 #pragma unroll
-                for (int kk = 0; kk < h; ++kk) ct_bfly<u64>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w, q, two_q);
+                for (int kk = 0; kk < h; ++kk) ct_bfly<W>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w, q, two_q);
             }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k) __stcs(reinterpret_cast<unsigned long long *>(p + (size_t)k * T), x[k]);
+        for (int k = 0; k < R; ++k) st_stream<W>(p + (size_t)k * T, x[k]);
     } else {
 #pragma unroll
         for (int sub = 0; sub < GS; ++sub) {
             const int hs = 1 << sub;
 #pragma unroll
             for (int v = 0; v < R / (2 * hs); ++v) {
-                const TwPair<u64> w = tw[(R >> (sub + 1)) + v];
+                const TwPair<W> w = tw[(R >> (sub + 1)) + v];
 #pragma unroll
-                for (int kk = 0; kk < hs; ++kk) gs_bfly<u64>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
+                for (int kk = 0; kk < hs; ++kk) gs_bfly<W>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], w, q, two_q);
             }
         }
-        const u64 ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
+        const W ni = a.ninv[2 * j], nip = a.ninv[2 * j + 1];
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-            __stcs(reinterpret_cast<unsigned long long *>(p + (size_t)k * T), csub(mul_shoup_lazy<u64>(x[k], ni, nip, q), q));
+        for (int k = 0; k < R; ++k) st_stream<W>(p + (size_t)k * T, csub(mul_shoup_lazy<W>(x[k], ni, nip, q), q));
     }
+}
+
+// Standalone MAC on u32 words (primes < 2^30): products < 2^60 accumulate exactly in u64
+// and are reduced every 15 terms (15 * 2^60 < 2^64); the per-split partial sums (< q)
+// are folded with 64-bit atomics into out64 [L][2][N], reduced by k_mac32_out.
+__global__ void __launch_bounds__(256) k_mac32(const u32 *__restrict__ ct, const u32 *__restrict__ pt, u32 D, u32 L,
+                                               u32 N, u32 dsplit, PrimeSet ps, u64 *__restrict__ out) {
+    const u32 pairs = (L * N) >> 1;
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= pairs) return;
+    const u32 lin = 2 * g, j = lin / N, i = lin % N;
+    const u64 q = ps.q[j];
+    const u32 per = (D + dsplit - 1) / dsplit;
+    const u32 d0 = blockIdx.y * per, d1 = min(D, d0 + per);
+    u64 a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+    u32 n = 0;
+    for (u32 d = d0; d < d1; ++d) {
+        const uint2 p = __ldcs(reinterpret_cast<const uint2 *>(pt + ((size_t)d * L + j) * N + i));
+        const uint2 c0 = __ldcs(reinterpret_cast<const uint2 *>(ct + (((size_t)d * L + j) * 2) * N + i));
+        const uint2 c1 = __ldcs(reinterpret_cast<const uint2 *>(ct + (((size_t)d * L + j) * 2 + 1) * N + i));
+        a00 += (u64)c0.x * p.x;
+        a01 += (u64)c0.y * p.y;
+        a10 += (u64)c1.x * p.x;
+        a11 += (u64)c1.y * p.y;
+        if (++n == 15) {
+            n = 0;
+            a00 %= q;
+            a01 %= q;
+            a10 %= q;
+            a11 %= q;
+        }
+    }
+    unsigned long long *o = reinterpret_cast<unsigned long long *>(out + (size_t)j * 2 * N + i);
+    atomicAdd(o, a00 % q);
+    atomicAdd(o + 1, a01 % q);
+    atomicAdd(o + N, a10 % q);
+    atomicAdd(o + N + 1, a11 % q);
+}
+
+__global__ void k_mac32_out(const u64 *__restrict__ acc, u32 L, u32 N, PrimeSet ps, u32 *__restrict__ out) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 2 * L * N) return;
+    out[i] = (u32)(acc[i] % ps.q[i / (2 * N)]);
 }
 
 // Standalone MAC: each thread owns 2 consecutive coefficients of one prime, loops over a d-range.
@@ -720,7 +777,7 @@ static cudaError_t pt_launch(const ephdc_ctx *c, const u32 *M, u32 nd, u64 *pt, 
     auto kern = k_plaintext_ntt<LG>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    kern<<<nd * c->L, (1 << LG) / kE, smem, st>>>(M, pt, mac_args(c));
+    kern<<<nd * c->L, (1 << LG) / batch_E<LG>(), smem, st>>>(M, pt, mac_args(c));
     return counted(cudaGetLastError());
 }
 
@@ -751,7 +808,7 @@ static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u64 d0, u32 nd, 
     a.cdt = c->dev.cdt;
     a.shat_mont = shat;
     a.tw = c->dev.tw_q;
-    kern<<<nd * c->L, (1 << LG) / kE, smem, st>>>(M, d0, a, model);
+    kern<<<nd * c->L, (1 << LG) / batch_E<LG>(), smem, st>>>(M, d0, a, model);
     return counted(cudaGetLastError());
 }
 
@@ -768,56 +825,62 @@ cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint64_t d0,
     return cudaErrorInvalidValue;
 }
 
-template <int LG, bool INV>
-static cudaError_t nttb_launch(const ephdc_ntt_plan *p, u64 *polys, u32 batch, cudaStream_t st) {
-    const size_t smem = sizeof(u64) * padded_len(1 << LG);
-    auto kern = k_ntt_batch<LG, INV>;
-    cudaError_t e = set_smem(kern, smem);
-    if (e != cudaSuccess) return e;
-    NttArgs a;
+template <typename W> static NttArgsW<W> ntt_args(const ephdc_ntt_plan *p, bool inv) {
+    NttArgsW<W> a;
     a.ps = p->ps;
     a.L = p->L;
     a.log2N = p->log2N;
-    a.tw = INV ? p->itw : p->tw;
-    a.ninv = p->ninv;
+    if constexpr (sizeof(W) == 8) {
+        a.tw = inv ? p->itw : p->tw;
+        a.ninv = p->ninv;
+    } else {
+        a.tw = inv ? p->itw32 : p->tw32;
+        a.ninv = p->ninv32;
+    }
+    return a;
+}
+
+template <int LG, bool INV, typename W>
+static cudaError_t nttb_launch(const ephdc_ntt_plan *p, W *polys, u32 batch, cudaStream_t st) {
+    const size_t smem = sizeof(W) * padded_len(1 << LG);
+    auto kern = k_ntt_batch<LG, INV, W>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
     const uint64_t grid = (uint64_t)batch * p->L << (p->log2N - LG);
     if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-    kern<<<(unsigned)grid, (1 << LG) / batch_E<LG>(), smem, st>>>(polys, a);
+    kern<<<(unsigned)grid, (1 << LG) / batch_E<LG>(), smem, st>>>(polys, ntt_args<W>(p, INV));
     return counted(cudaGetLastError());
 }
 
-template <int GS, bool INV>
-static cudaError_t nttg_launch(const ephdc_ntt_plan *p, u64 *polys, u32 batch, cudaStream_t st) {
-    NttArgs a;
-    a.ps = p->ps;
-    a.L = p->L;
-    a.log2N = p->log2N;
-    a.tw = INV ? p->itw : p->tw;
-    a.ninv = p->ninv;
+template <int GS, bool INV, typename W>
+static cudaError_t nttg_launch(const ephdc_ntt_plan *p, W *polys, u32 batch, cudaStream_t st) {
     const uint64_t n_polys = (uint64_t)batch * p->L;
     const uint64_t threads = n_polys * (p->N >> GS);
     const uint64_t blocks = (threads + 255) / 256;
     if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-    k_ntt_global<GS, INV><<<(unsigned)blocks, 256, 0, st>>>(polys, (u32)n_polys, a);
+    k_ntt_global<GS, INV, W><<<(unsigned)blocks, 256, 0, st>>>(polys, (u32)n_polys, ntt_args<W>(p, INV));
     return counted(cudaGetLastError());
 }
 
-template <bool INV>
-static cudaError_t ntt_large(const ephdc_ntt_plan *p, u64 *polys, u32 batch, cudaStream_t st) {
+template <bool INV, typename W>
+static cudaError_t ntt_large(const ephdc_ntt_plan *p, W *polys, u32 batch, cudaStream_t st) {
     // forward: global stages, then 2^14-point slices; inverse: slices, then global stages
     cudaError_t e = cudaSuccess;
-    if (!INV) e = p->log2N == 15 ? nttg_launch<1, false>(p, polys, batch, st) : nttg_launch<2, false>(p, polys, batch, st);
+    if (!INV)
+        e = p->log2N == 15 ? nttg_launch<1, false, W>(p, polys, batch, st) : nttg_launch<2, false, W>(p, polys, batch, st);
     if (e != cudaSuccess) return e;
-    e = nttb_launch<14, INV>(p, polys, batch, st);
+    e = nttb_launch<14, INV, W>(p, polys, batch, st);
     if (e != cudaSuccess || !INV) return e;
-    return p->log2N == 15 ? nttg_launch<1, true>(p, polys, batch, st) : nttg_launch<2, true>(p, polys, batch, st);
+    return p->log2N == 15 ? nttg_launch<1, true, W>(p, polys, batch, st) : nttg_launch<2, true, W>(p, polys, batch, st);
 }
 
-cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
-                             cudaStream_t st) {
+template <typename W>
+static cudaError_t ntt_batch_w(const ephdc_ntt_plan *p, W *d_polys, uint32_t batch, bool inverse, cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
-#define EPHDC_NTTB(LG) \
-    case LG: return inverse ? nttb_launch<LG, true>(p, d_polys, batch, st) : nttb_launch<LG, false>(p, d_polys, batch, st);
+#define EPHDC_NTTB(LG)                                                             \
+    case LG:                                                                       \
+        return inverse ? nttb_launch<LG, true, W>(p, d_polys, batch, st)          \
+                       : nttb_launch<LG, false, W>(p, d_polys, batch, st);
     switch (p->log2N) {
         EPHDC_NTTB(10)
         EPHDC_NTTB(11)
@@ -825,10 +888,46 @@ cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_
         EPHDC_NTTB(13)
         EPHDC_NTTB(14)
         case 15:
-        case 16: return inverse ? ntt_large<true>(p, d_polys, batch, st) : ntt_large<false>(p, d_polys, batch, st);
+        case 16: return inverse ? ntt_large<true, W>(p, d_polys, batch, st) : ntt_large<false, W>(p, d_polys, batch, st);
     }
 #undef EPHDC_NTTB
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ntt_batch(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
+                             cudaStream_t st) {
+    return ntt_batch_w<u64>(p, d_polys, batch, inverse, st);
+}
+
+cudaError_t launch_ntt_batch32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, bool inverse,
+                               cudaStream_t st) {
+    if (!p->tw32) return cudaErrorInvalidValue;
+    return ntt_batch_w<u32>(p, d_polys, batch, inverse, st);
+}
+
+cudaError_t launch_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,
+                         uint32_t *d_out, cudaStream_t st) {
+    const u32 L = p->L, N = p->N;
+    u64 *acc = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&acc), sizeof(u64) * 2 * L * N, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(acc, 0, sizeof(u64) * 2 * L * N, st);
+    const u32 pairs = (L * N) / 2;
+    const u32 bx = (pairs + 255) / 256;
+    // <= 2^16 partial sums < q < 2^30 per coefficient: the 64-bit fold cannot wrap
+    u32 dsplit = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
+    dsplit = std::max<u32>(1, std::min(std::min(dsplit, D), 1u << 16));
+    if (e == cudaSuccess && D > 0) {
+        k_mac32<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, acc);
+        e = counted(cudaGetLastError());
+    }
+    if (e == cudaSuccess) {
+        const u32 n = 2 * L * N;
+        k_mac32_out<<<(n + 255) / 256, 256, 0, st>>>(acc, L, N, p->ps, d_out);
+        e = counted(cudaGetLastError());
+    }
+    const cudaError_t e2 = cudaFreeAsync(acc, st);
+    return e != cudaSuccess ? e : e2;
 }
 
 cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,

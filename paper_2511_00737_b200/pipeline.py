@@ -1,8 +1,9 @@
 """Config-level setup of the product path: parameters, model build, keys, encrypted model.
 
 Used by bench.py, __graft_entry__.smoke() and the GPU tests.  Primes and psi come
-from the library (ephdc_find_ntt_primes / ctx_create), training from model.py, and
-every device step from libephdc kernels.
+from the library (ephdc_find_ntt_primes / ctx_create), the model build from
+ephdc_query_bits / ephdc_train_model (host C++), every device step from libephdc
+kernels; this module only sequences the calls.
 """
 from __future__ import annotations
 
@@ -12,8 +13,7 @@ from typing import Optional
 import numpy as np
 
 import ephdc_inputs as inp
-from . import Context, EncryptedModel, SecretKey, Workspace, encode_raw, find_ntt_primes
-from . import model as model_build
+from . import Context, EncryptedModel, SecretKey, encode_raw, find_ntt_primes, query_bits, train_model
 
 SK_SEED_OFFSET = 17      # same seed schedule as the oracle's driver (inputs, not arithmetic)
 ENC_SEED_OFFSET = 29
@@ -55,14 +55,14 @@ def build(cfg: inp.Config, P: np.ndarray, X_train: np.ndarray, y_train: np.ndarr
     import torch
     dev = torch.device("cuda", device)
     t, q = primes_for(cfg)
-    Qbits = model_build.query_bits(cfg.D_live, cfg.Cbits, t)
+    Qbits = query_bits(cfg.D_live, cfg.Cbits, t)
     P_dev = torch.from_numpy(np.ascontiguousarray(P)).to(dev)
     # training projection on the GPU (the quantisation fields are unused by encode_raw)
     ctx0 = make_context(cfg, t, q, Qbits, 0, device, arith, encoder)
     Xt = torch.from_numpy(np.ascontiguousarray(X_train).view(np.int8)).to(dev)
     acc = encode_raw(ctx0, Xt, P_dev).cpu().numpy()
     torch.cuda.synchronize(dev)
-    class_hv, qshift = model_build.train(acc, y_train, cfg.k, cfg.Cbits, Qbits)
+    class_hv, qshift = train_model(acc, y_train, cfg.k, cfg.Cbits, Qbits)
     ctx0.close()
     ctx = make_context(cfg, t, q, Qbits, qshift, device, arith, encoder)
     sk = SecretKey(ctx, cfg.seed + SK_SEED_OFFSET if sk_seed is None else sk_seed)

@@ -14,7 +14,7 @@ from oracle.bfv import OracleBFV, gaussian_cdt as oracle_cdt
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 import paper_2511_00737_b200 as eph  # noqa: E402
-from paper_2511_00737_b200 import _capi, model as pmodel  # noqa: E402
+from paper_2511_00737_b200 import _capi  # noqa: E402
 
 
 def _header_symbols():
@@ -136,8 +136,8 @@ def test_product_model_build_matches_oracle():
         P = inp.gen_projection(cfg)
         bfv = OracleBFV(cfg)
         Q = hdc.choose_Qbits(cfg.D_live, cfg.Cbits, bfv.t)
-        assert pmodel.query_bits(cfg.D_live, cfg.Cbits, bfv.t) == Q
+        assert eph.query_bits(cfg.D_live, cfg.Cbits, bfv.t) == Q
         acc = hdc.encode_raw(P, Xtr, cfg.D_live)   # input to both sides
-        C, s = pmodel.train(acc, ytr, cfg.k, cfg.Cbits, Q)
+        C, s = eph.train_model(acc, ytr, cfg.k, cfg.Cbits, Q)
         assert s == hdc.calibrate_shift(acc, Q)
         assert np.array_equal(C, hdc.quantise_classes(hdc.bundle(acc, ytr, cfg.k), cfg.Cbits))

@@ -105,3 +105,41 @@ def test_ntt_c5_prime_switch(log2N, L, bits, batch):
             assert np.array_equal(got[b, j], core.ntt_fwd(x[b, j][None, :], log2N, q[j], psi)[0]), (b, j)
     eph.ntt_inv(plan, d)
     assert np.array_equal(_host(d), x)
+
+
+@pytest.mark.parametrize("log2N", [10, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("L", [1, 5, 16])
+def test_ntt_u32_words(log2N, L):
+    """30-bit primes on u32 words (ephdc_ntt_fwd32 / inv32 / mac32) bit-exact."""
+    N = 1 << log2N
+    q = nt.prime_chain([30] * L, log2N)
+    x = inp.gen_residues(q, 3, N, seed=log2N + 31 * L)
+    plan = eph.NttPlan(q, log2N)
+    assert plan.u32_words
+    d = torch.from_numpy(x.astype(np.int32)).cuda()
+    eph.ntt_fwd32(plan, d)
+    got = d.cpu().numpy().astype(np.uint64)
+    for j, p in enumerate(q):
+        psi = nt.min_primitive_2n_root(p, N)
+        assert np.array_equal(got[:, j, :], core.ntt_fwd(x[:, j, :], log2N, p, psi)), j
+    eph.ntt_inv32(plan, d)
+    assert np.array_equal(d.cpu().numpy().astype(np.uint64), x)
+    D = 37
+    ct = np.stack([inp.gen_residues(q, D, N, seed=1), inp.gen_residues(q, D, N, seed=2)], axis=2)   # [D][L][2][N]
+    pt = inp.gen_residues(q, D, N, seed=3)
+    out = eph.mac32(plan, torch.from_numpy(ct.astype(np.int32)).cuda(), torch.from_numpy(pt.astype(np.int32)).cuda())
+    out = out.cpu().numpy().astype(np.uint64)
+    for j, p in enumerate(q):
+        for c in range(2):
+            acc = np.zeros(N, dtype=object)
+            for dd in range(D):
+                acc = (acc + ct[dd, j, c].astype(object) * pt[dd, j].astype(object)) % p
+            assert np.array_equal(out[j, c], acc.astype(np.uint64)), (j, c)
+
+
+def test_u32_words_need_small_primes():
+    q = nt.prime_chain([48], 12)
+    plan = eph.NttPlan(q, 12)
+    assert not plan.u32_words
+    with pytest.raises(eph.EphdcError):
+        eph.ntt_fwd32(plan, torch.zeros((1, 1, 4096), dtype=torch.int32, device="cuda"))

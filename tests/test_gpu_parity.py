@@ -160,3 +160,27 @@ def test_launch_counter_increases():
     eph.infer_batch(r["ps"].ctx, r["ps"].model, ws, r["H_dev"], 16)
     torch.cuda.synchronize()
     assert eph.launch_count() - n0 == 3      # pack_intt, ntt_mac, finalize for one batch
+
+
+@pytest.mark.parametrize("k,nq", [(1, 700), (1, 1024 + 3), (3, 341 * 2 + 5)])
+def test_slot_packing_small_k(k, nq):
+    """k = 1 (one query per slot: the slot -> query division is the identity) and k = 3
+    (B = 341, a ragged 1024 = 3 * 341 + 1 tail slot): scores ciphertexts bit-exact with
+    the oracle, decryption = brute-force dot products (k = 1)."""
+    import dataclasses
+    cfg = dataclasses.replace(inp.CONFIGS["c1q3"], name=f"c1q3k{k}", k=k)
+    Xtr, ytr, Xq, _ = inp.gen_features(cfg, nq)
+    P = inp.gen_projection(cfg)
+    om = opipe.build_model(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr)
+    X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
+    H = eph.encode_queries(ps.ctx, X, ps.P_dev)
+    ws = eph.Workspace(ps.ctx, nq)
+    got = _u64(eph.infer_batch(ps.ctx, ps.model, ws, H, nq))
+    H_or = opipe.encode_queries(om, P, Xq)
+    assert np.array_equal(H.cpu().numpy(), H_or)
+    assert np.array_equal(got, opipe.infer_all(om, H_or))
+    S, lab = eph.decrypt_scores(ps.ctx, ps.sk, got, nq)
+    Sref = hdc.scores(H_or, om.class_hv)
+    assert np.array_equal(S, Sref)
+    assert np.array_equal(lab.astype(np.int64), hdc.argmax_lowest(Sref))

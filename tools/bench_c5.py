@@ -1,14 +1,18 @@
 #!/usr/bin/env python
 """c5 kernel microbench (BASELINE.json configs[4]): standalone negacyclic NTT (forward,
-inverse) and the pointwise ct x pt MAC on uniform residues, one JSON line per point.
+inverse) and the pointwise ct x pt MAC on uniform residues, one JSON line per
+(N, L, prime class, word, batch) point -- the points of ephdc_inputs.c5_points, each
+one parity-checked by tests/test_gpu_c5_sweep.py on the same seeded device inputs.
 
-GB/s = algorithmic bytes / CUDA-event time on the launching stream:
-  NTT: read + write of batch x L x N u64 residues (in place);
-  MAC: read of D x L x (2 + 1) x N u64 (two ciphertext residues + one plaintext).
-Working sets are >= 1 GiB (8x L2) so every timed repetition streams from HBM.
+GB/s = algorithmic bytes / CUDA-event time on the launching stream (warm-up first):
+  NTT: read + write of batch x L x N words (in place);
+  MAC: read of D x L x (2 + 1) x N words (two ciphertext residues + one plaintext).
+Small batches are latency-bound by construction (one polynomial per prime cannot fill
+148 SMs); working sets above 1 GiB stream from HBM (L2 = 126 MB).  Every line carries
+the nvidia-smi clock record of its timed region (bench.ClockSampler).
 Peak: MEASURED_PEAKS.json hbm_gbs.
 
-usage: python tools/bench_c5.py [--points quick|all] [--reps 5]
+usage: python tools/bench_c5.py [--points quick|all] [--reps 5] [--only 13:9:48:8]
 """
 from __future__ import annotations
 
@@ -16,8 +20,6 @@ import argparse
 import json
 import os
 import sys
-
-import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -27,67 +29,77 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--points", default="quick", choices=["quick", "all"])
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--bytes", type=float, default=2.0, help="GiB working set per point")
+    ap.add_argument("--only", default="", help="lg:L:bits:wordbytes[,...]")
+    ap.add_argument("--max-batch-only", action="store_true", help="time only the largest batch of each point")
     a = ap.parse_args()
     import torch
     import ephdc_inputs as inp
     import paper_2511_00737_b200 as eph
+    from bench import ClockSampler, measured_peaks
 
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm = peaks.get("hbm_gbs", 6460.5)
-    if a.points == "quick":
-        pts = [(lg, L, b) for lg in (12, 13, 14, 15, 16) for L, b in ((9, 48), (5, 60), (16, 30))]
-    else:
-        pts = [(lg, L, b) for lg in inp.C5_LOG2N for L in inp.C5_L for b in inp.C5_WORD_BITS]
+    hbm = measured_peaks().get("hbm_gbs", 6552.0)
+    only = {tuple(int(v) for v in s.split(":")) for s in a.only.split(",") if s}
     dev = torch.device("cuda", 0)
-    for lg, L, bits in pts:
-        N = 1 << lg
-        q = eph.find_ntt_primes(lg, [bits] * L)
-        plan = eph.NttPlan(q, lg)
-        per_poly = L * N * 8
-        batch = max(1, int(a.bytes * (1 << 30) // per_poly))
-        x = torch.randint(0, 1 << 62, (batch, L, N), dtype=torch.int64, device=dev)
-        qt = torch.tensor([int(v) for v in q], dtype=torch.int64, device=dev).view(1, L, 1)
-        x = torch.remainder(x, qt)
-        res = {}
-        for name, fn in (("ntt_fwd", eph.ntt_fwd), ("ntt_inv", eph.ntt_inv)):
-            for _ in range(3):
-                fn(plan, x)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(a.reps):
-                fn(plan, x)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / a.reps
-            gbs = 2 * batch * per_poly / (ms / 1e3) / 1e9
-            res[name] = {"ms": round(ms, 4), "GB_s": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4),
-                         "butterflies_G_s": round(batch * L * (N // 2) * lg / (ms / 1e3) / 1e9, 1)}
-        # MAC: D terms of ct [D][L][2][N] and pt [D][L][N]
-        D = max(1, int(a.bytes * (1 << 30) // (3 * per_poly)))
-        ct = torch.remainder(torch.randint(0, 1 << 62, (D, L, 2, N), dtype=torch.int64, device=dev), qt.view(1, L, 1, 1))
-        pt = torch.remainder(torch.randint(0, 1 << 62, (D, L, N), dtype=torch.int64, device=dev), qt)
-        out = torch.empty((L, 2, N), dtype=torch.int64, device=dev)
-        for _ in range(3):
-            eph.mac(plan, ct, pt, out)
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(a.reps):
-            eph.mac(plan, ct, pt, out)
+        for _ in range(reps):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / a.reps
+        return e0.elapsed_time(e1) / reps
+
+    for lg, L, bits, wb, batches in inp.c5_points(a.points):
+        if only and (lg, L, bits, wb) not in only:
+            continue
+        N = 1 << lg
+        q = eph.find_ntt_primes(lg, [bits] * L)
+        plan = eph.NttPlan(q, lg)
+        if wb == 4 and not plan.u32_words:
+            continue
+        fwd, inv, mac = (eph.ntt_fwd, eph.ntt_inv, eph.mac) if wb == 8 else (eph.ntt_fwd32, eph.ntt_inv32, eph.mac32)
+        dt = torch.int64 if wb == 8 else torch.int32
+        seed = lg * 1000 + L * 10 + bits + wb
+        base = inp.c5_residues_torch(q, max(batches), N, seed, dev, dt)
+        per_poly = L * N * wb
+        for batch in (batches[-1:] if a.max_batch_only else batches):
+            x = base[:batch]
+            reps = a.reps if batch * per_poly >= (1 << 28) else max(a.reps, 50)
+            clk = ClockSampler(0)
+            clk.start()
+            res = {}
+            for name, fn in (("ntt_fwd", fwd), ("ntt_inv", inv)):
+                ms = timed(lambda: fn(plan, x), reps)
+                gbs = 2 * batch * per_poly / (ms / 1e3) / 1e9
+                res[name] = {"ms": round(ms, 5), "GB_s": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4),
+                             "butterflies_G_s": round(batch * L * (N // 2) * lg / (ms / 1e3) / 1e9, 1)}
+            res["clocks"] = clk.stop()
+            res["kernels"] = {"fwd": plan.fwd_kernel if wb == 8 else "int_u32",
+                              "inv": plan.inv_kernel if wb == 8 else "int_u32"}
+            print(json.dumps({"workload": "c5", "log2N": lg, "L": L, "bits": bits, "word_bits": 8 * wb,
+                              "batch": batch, "bytes_per_launch": 2 * batch * per_poly, "hbm_peak_gbs": hbm,
+                              **res}), flush=True)
+        del base
+        torch.cuda.empty_cache()
+        # MAC: D terms of ct [D][L][2][N] and pt [D][L][N] (~2 GiB)
+        D = max(1, min(inp.c5_max_batch(lg, L, wb), (2 << 30) // (3 * per_poly)))
+        mods = [q[j] for j in range(L) for _ in range(2)]
+        ct = inp.c5_residues_torch(mods, D, N, seed + 1, dev, dt).view(D, L, 2, N)
+        pt = inp.c5_residues_torch(q, D, N, seed + 2, dev, dt)
+        out = torch.empty((L, 2, N), dtype=dt, device=dev)
+        clk = ClockSampler(0)
+        clk.start()
+        ms = timed(lambda: mac(plan, ct, pt, out), a.reps)
+        c = clk.stop()
         gbs = 3 * D * per_poly / (ms / 1e3) / 1e9
-        res["mac"] = {"D": D, "ms": round(ms, 4), "GB_s": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
-        print(json.dumps({"workload": "c5", "log2N": lg, "L": L, "bits": bits, "batch": batch,
-                          "hbm_peak_gbs": hbm, **res}), flush=True)
-        del x, ct, pt, out
+        print(json.dumps({"workload": "c5", "op": "mac", "log2N": lg, "L": L, "bits": bits, "word_bits": 8 * wb,
+                          "D": D, "ms": round(ms, 4), "GB_s": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4),
+                          "hbm_peak_gbs": hbm, "clocks": c}), flush=True)
+        del ct, pt, out
         torch.cuda.empty_cache()
 
 
