@@ -257,6 +257,15 @@ ephdc_status ephdc_infer_batch(const ephdc_ctx *ctx, const ephdc_model *model, e
                                const int8_t *d_H, uint32_t nq, uint64_t *d_out, uint32_t cap_ct,
                                void *stream);
 
+/* findDmax's evaluation (Algorithm 1 l.20: evalHEcomputation(N, T, D)):
+ * ephdc_infer_batch where batch b sums only its first h_dims[b] dims (host array
+ * [ceil(nq/B)], each <= D_live) -- the same kernels, so 1000 trials of different
+ * lengths are one call.  Errors as ephdc_infer_batch, EPARAM if a count exceeds
+ * D_live or nq exceeds the workspace.  Async (h_dims is consumed before return). */
+ephdc_status ephdc_infer_batch_prefix(const ephdc_ctx *ctx, const ephdc_model *model, ephdc_workspace *ws,
+                                      const int8_t *d_H, uint32_t nq, const uint32_t *h_dims, uint64_t *d_out,
+                                      uint32_t cap_ct, void *stream);
+
 /* Intermediate export for parity tests: the plaintext NTTs p_hat_{b,d,j} of
  * batch b for dims [d0, d0+nd): d_pt [nd][L][N] canonical.  Async. */
 ephdc_status ephdc_encode_plaintexts(const ephdc_ctx *ctx, ephdc_workspace *ws, const int8_t *d_H,

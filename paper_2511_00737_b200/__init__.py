@@ -19,7 +19,7 @@ from ._capi import EphdcError, call, lib
 __all__ = [
     "Context", "SecretKey", "EncryptedModel", "Workspace", "NttPlan", "EphdcError",
     "find_ntt_primes", "min_psi", "gaussian_cdt", "query_bits", "train_model", "launch_count",
-    "encode_queries", "encode_raw", "infer_batch", "encode_plaintexts", "classify_host",
+    "encode_queries", "encode_raw", "infer_batch", "infer_batch_prefix", "encode_plaintexts", "classify_host",
     "scores_message_bytes", "pack_scores", "unpack_scores", "classify_host_packed",
     "sr_encrypt_queries", "sr_model_plaintexts", "sr_evaluate",
     "decrypt_scores", "decrypt_slots", "ntt_fwd", "ntt_inv", "mac", "ntt_fwd32", "ntt_inv32", "mac32",
@@ -264,6 +264,19 @@ def infer_batch(ctx: Context, model: EncryptedModel, ws: Workspace, H, nq: Optio
         out = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, device=H.device)
     call("ephdc_infer_batch", ctx.handle, model.handle, ws.handle, _dptr(H), nq, _dptr(out), out.shape[0],
          _stream(stream))
+    return out
+
+
+def infer_batch_prefix(ctx: Context, model: EncryptedModel, ws: Workspace, H, nq: int, dims, out=None, stream=None):
+    """ephdc_infer_batch_prefix: batch b sums its first dims[b] dims (findDmax's evaluation)."""
+    import torch
+    nb = ctx.n_batches(nq)
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.uint32))
+    assert d.size == nb
+    if out is None:
+        out = torch.empty(ctx.ct_shape(nq), dtype=torch.int64, device=H.device)
+    call("ephdc_infer_batch_prefix", ctx.handle, model.handle, ws.handle, _dptr(H), nq, _np_ptr(d), _dptr(out),
+         out.shape[0], _stream(stream))
     return out
 
 

@@ -79,6 +79,7 @@ _SIGS = {
     "ephdc_encode_queries": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
     "ephdc_encode_raw": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
     "ephdc_infer_batch": (c_st, [c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_u32, c_vp]),
+    "ephdc_infer_batch_prefix": (c_st, [c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_vp, c_u32, c_vp]),
     "ephdc_encode_plaintexts": (c_st, [c_vp, c_vp, c_vp, c_u32, c_u32, c_u32, c_u32, c_vp, c_vp]),
     "ephdc_classify_host": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_u32, c_vp]),
     "ephdc_decrypt_scores": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),

@@ -484,6 +484,7 @@ void ephdc_workspace_free(ephdc_workspace *ws) {
     cudaFree(ws->d_H);
     cudaFree(ws->d_out);
     cudaFree(ws->d_msg);
+    cudaFree(ws->d_dlim);
     for (cudaEvent_t e : ws->ev_pool) cudaEventDestroy(e);
     delete ws;
 }
@@ -515,7 +516,8 @@ ephdc_status ephdc_workspace_create(const ephdc_ctx *c, uint32_t max_nq, const e
     if (dev_alloc(&ws->d_M, D * c->N * ws->m_batches) != cudaSuccess || cudaMalloc(&ws->d_X, (size_t)max_nq * c->p.F) != cudaSuccess ||
         dev_alloc(&ws->d_H, D * max_nq) != cudaSuccess ||
         dev_alloc(&ws->d_out, (size_t)ws->nb_max * 2 * c->L * c->N) != cudaSuccess ||
-        dev_alloc(&ws->d_msg, ephdc_scores_message_bytes(c, ws->nb_max)) != cudaSuccess) {
+        dev_alloc(&ws->d_msg, ephdc_scores_message_bytes(c, ws->nb_max)) != cudaSuccess ||
+        dev_alloc(&ws->d_dlim, ws->nb_max) != cudaSuccess) {
         ephdc_workspace_free(ws.release());
         return EPHDC_ERESOURCE;
     }
@@ -585,11 +587,13 @@ ephdc_status ephdc_encode_raw(const ephdc_ctx *c, const void *d_X, const int8_t 
 }
 
 static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws, const int8_t *d_H,
-                               uint32_t nq, uint64_t *d_out, cudaStream_t st) {
+                               uint32_t nq, uint64_t *d_out, cudaStream_t st, const uint32_t *h_dims = nullptr) {
     const uint32_t nb = (nq + c->B - 1) / c->B;
     const size_t per = (size_t)2 * c->L * c->N;
     if (nb == 0) return EPHDC_OK;
     EPHDC_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(uint64_t) * per * nb, st));
+    if (h_dims && c->f64.enabled)   // per-batch dim counts for the fused kernel (pageable copy: synchronous)
+        EPHDC_CUDA_TRY(cudaMemcpyAsync(ws->d_dlim, h_dims, sizeof(uint32_t) * nb, cudaMemcpyHostToDevice, st));
     if (c->f64.enabled) {
         // FP64 path: pack + INTT_t of a group of batches, then ONE fused launch over the group
         for (uint32_t b0 = 0; b0 < nb; b0 += ws->m_batches) {
@@ -601,7 +605,8 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
             }
             {
                 Timer tm(ws, st, kClsMac);
-                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->plan, ws->d_M, g, reinterpret_cast<const double *>(m->d_ct), d_out + per * b0, st));
+                EPHDC_CUDA_TRY(launch_ntt_mac_f64(c, ws->plan, ws->d_M, g, reinterpret_cast<const double *>(m->d_ct),
+                                                  d_out + per * b0, st, h_dims ? ws->d_dlim + b0 : nullptr));
                 tm.done();
             }
         }
@@ -619,7 +624,7 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
         }
         {
             Timer tm(ws, st, kClsMac);
-            EPHDC_CUDA_TRY(launch_ntt_mac(c, ws->d_M, m->d_ct, d_out + per * b, st));
+            EPHDC_CUDA_TRY(launch_ntt_mac(c, ws->d_M, m->d_ct, d_out + per * b, st, h_dims ? h_dims[b] : 0xffffffffu));
             tm.done();
         }
         {
@@ -640,6 +645,20 @@ ephdc_status ephdc_infer_batch(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
     if (cap_ct < nb) return EPHDC_EOVERFLOW;
     EPHDC_CUDA_TRY(cudaSetDevice(c->device));
     return infer_impl(c, m, ws, d_H, nq, d_out, (cudaStream_t)stream);
+}
+
+ephdc_status ephdc_infer_batch_prefix(const ephdc_ctx *c, const ephdc_model *m, ephdc_workspace *ws,
+                                      const int8_t *d_H, uint32_t nq, const uint32_t *h_dims, uint64_t *d_out,
+                                      uint32_t cap_ct, void *stream) {
+    if (!c || !m || !ws || ((!d_H || !d_out || !h_dims) && nq)) return EPHDC_ENULL;
+    if (m->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
+    const uint32_t nb = (nq + c->B - 1) / c->B;
+    if (cap_ct < nb) return EPHDC_EOVERFLOW;
+    if (nq > ws->max_nq) return EPHDC_EPARAM;
+    for (uint32_t b = 0; b < nb; ++b)
+        if (h_dims[b] > c->p.D_live) return EPHDC_EPARAM;
+    EPHDC_CUDA_TRY(cudaSetDevice(c->device));
+    return infer_impl(c, m, ws, d_H, nq, d_out, (cudaStream_t)stream, h_dims);
 }
 
 ephdc_status ephdc_encode_plaintexts(const ephdc_ctx *c, ephdc_workspace *ws, const int8_t *d_H, uint32_t nq,
@@ -830,23 +849,35 @@ ephdc_status ephdc_decrypt_scores(const ephdc_ctx *c, const ephdc_sk *sk, const 
     const uint32_t N = c->N, k = c->p.k, B = c->B;
     const uint32_t nb = (nq + B - 1) / B;
     const int64_t t = (int64_t)c->t;
-    std::vector<uint64_t> slots(N);
-    for (uint32_t b = 0; b < nb; ++b) {
-        decrypt_one(c, sk, h_ct + (size_t)b * 2 * c->L * N, slots.data());
-        const uint32_t n_b = std::min(B, nq - b * B);
-        for (uint32_t qi = 0; qi < n_b; ++qi) {
-            const uint32_t qg = b * B + qi;
-            int64_t best = 0;
-            uint32_t arg = 0;
-            for (uint32_t cl = 0; cl < k; ++cl) {
-                int64_t v = (int64_t)slots[(size_t)qi * k + cl];
-                if (v > (t - 1) / 2) v -= t;
-                h_scores[(size_t)qg * k + cl] = v;
-                if (cl == 0 || v > best) { best = v; arg = cl; }
+    // batches are independent ciphertexts: host threads over them (the NTT tables and the
+    // CRT context are read-only)
+    auto work = [&](uint32_t b0, uint32_t b1) {
+        std::vector<uint64_t> slots(N);
+        for (uint32_t b = b0; b < b1; ++b) {
+            decrypt_one(c, sk, h_ct + (size_t)b * 2 * c->L * N, slots.data());
+            const uint32_t n_b = std::min(B, nq - b * B);
+            for (uint32_t qi = 0; qi < n_b; ++qi) {
+                const uint32_t qg = b * B + qi;
+                int64_t best = 0;
+                uint32_t arg = 0;
+                for (uint32_t cl = 0; cl < k; ++cl) {
+                    int64_t v = (int64_t)slots[(size_t)qi * k + cl];
+                    if (v > (t - 1) / 2) v -= t;
+                    h_scores[(size_t)qg * k + cl] = v;
+                    if (cl == 0 || v > best) { best = v; arg = cl; }
+                }
+                if (h_labels) h_labels[qg] = arg;
             }
-            if (h_labels) h_labels[qg] = arg;
         }
+    };
+    const uint32_t nt = std::max<uint32_t>(1, std::min<uint32_t>(nb, std::thread::hardware_concurrency()));
+    if (nt <= 1) {
+        work(0, nb);
+        return EPHDC_OK;
     }
+    std::vector<std::thread> pool;
+    for (uint32_t i = 0; i < nt; ++i) pool.emplace_back(work, (uint32_t)((uint64_t)nb * i / nt), (uint32_t)((uint64_t)nb * (i + 1) / nt));
+    for (auto &th : pool) th.join();
     return EPHDC_OK;
 }
 
@@ -904,10 +935,6 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
     }
     plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
     if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
-    for (uint32_t j = 0; j < L; ++j) {
-        p->c5_w1[j] = tw[(size_t)j * N + 1].w;
-        p->c5_w1p[j] = tw[(size_t)j * N + 1].wp;
-    }
 
     if (p->fwd_f64 || p->inv_f64) {
         // FP64 tables: forward psi_rev; inverse = Cooley-Tukey DIT on the bit-reversed

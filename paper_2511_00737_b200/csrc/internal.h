@@ -35,6 +35,7 @@ struct F64MacArgs {
     u32 chunks, G;           // dim chunks per batch, dims per chunk
     u32 red_every;           // accumulator reduction interval (dims)
     u32 flags;               // bit 0 = no explicit L2 prefetch of the model slice (launch plan)
+    const u32 *dlim;         // [nb] dims summed per batch (ephdc_infer_batch_prefix), or null = D
 };
 
 // FP64 path plan: chosen at context creation when every q_j < 2^50 and the value
@@ -105,6 +106,7 @@ struct ephdc_workspace {
     int8_t *d_H = nullptr;        // [D_live][max_nq]
     uint64_t *d_out = nullptr;    // [nb_max][2][L][N]
     uint8_t *d_msg = nullptr;     // packed scores message of nb_max ciphertexts
+    uint32_t *d_dlim = nullptr;   // [nb_max] per-batch dim counts (ephdc_infer_batch_prefix)
     uint32_t nb_max = 0;
     ephdc_plan plan{};            // launch-plan overrides (tests/profiling; zeros = tuned)
     // timing
@@ -135,15 +137,13 @@ struct ephdc_ntt_plan {
     // 0 = (q, 1/q); the inverse's scaling: GS N^-1 [L], DIT N^-1 psi^-j [L][N] (w, w/q)
     double2 *tw_f64 = nullptr, *itw_f64 = nullptr;
     double2 *post_f64 = nullptr;
-    // c5 kernels (ntt_c5.cu) when their bounds hold: level-0 twiddle psi_rev[1] with its
-    // Shoup companion, Barrett constants floor(2^64/q) and the offset K q of the final
-    // reduction, per prime
-    bool c5_fwd = false, c5_inv = false;
-    uint64_t c5_w1[EPHDC_MAX_PRIMES]{}, c5_w1p[EPHDC_MAX_PRIMES]{};
-    uint64_t c5_bm[EPHDC_MAX_PRIMES]{}, c5_off[EPHDC_MAX_PRIMES]{};
+    // c5 kernels (ntt_c5.cu) when their bounds hold; c5_red: a cluster forward reduces
+    // after its cross levels
+    bool c5_fwd = false, c5_inv = false, c5_red = false;
     // inverse: DIT table [L][N] (W[h + jj] = omega^-(N/2h) jj, entry 0 = (q, 1/q)), fused
-    // last-level scaling [L][N/2][2] (s_j, s_j W[N/2 + j]), s_j = N^-1 psi^-j; c = psi^-N/2
-    double2 *c5_itw = nullptr, *c5_itail = nullptr;
+    // level-12 scaling [L][NC/2][2] (sigma_r, sigma_r W[NC/2 + r]), sigma_r = N^-1 psi^-r;
+    // c_loc = psi^-(NC/2); block constants c_k = psi^-(NC k) [L][8]
+    double2 *c5_itw = nullptr, *c5_itail = nullptr, *c5_ck = nullptr;
     double2 c5_cinv[EPHDC_MAX_PRIMES]{};
 };
 
@@ -160,7 +160,7 @@ cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint
 cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
                                    cudaStream_t st);
 cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64_t *d_model, uint64_t *d_out,
-                           cudaStream_t st);
+                           cudaStream_t st, uint32_t d_lim = 0xffffffffu);
 cudaError_t launch_finalize(const ephdc_ctx *c, uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
                                  cudaStream_t st);
@@ -187,7 +187,8 @@ cudaError_t launch_encode_tc(const ephdc_ctx *c, const void *d_X, const int8_t *
                              cudaStream_t st);
 // FP64-pipe path (kernels_f64.cu)
 cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const ephdc_plan &plan, const uint32_t *d_M, uint32_t nb,
-                               const double *d_model, uint64_t *d_out, cudaStream_t st);
+                               const double *d_model, uint64_t *d_out, cudaStream_t st,
+                               const uint32_t *d_dlim = nullptr);
 cudaError_t launch_u64_to_f64(uint64_t *d, size_t n, cudaStream_t st);
 // scores message layout (bit-packed residues, ephdc.h "scores message")
 struct MsgLayout {
@@ -218,9 +219,10 @@ struct C5Args {
     const double2 *tw;     // forward: [L][N] (psi_rev[i], fl(psi_rev[i]/q_j)), entry 0 = (q_j, fl(1/q_j));
                            // inverse: the DIT table ephdc_ntt_plan::c5_itw
     const double2 *tail;   // inverse: ephdc_ntt_plan::c5_itail
+    const double2 *ck;     // inverse: ephdc_ntt_plan::c5_ck
     u32 L, batch, items;   // items = L * batch (prime-major work order)
-    u64 q[kMaxL], w1[kMaxL], w1p[kMaxL], bm[kMaxL], off[kMaxL];
-    double2 cinv[kMaxL];   // inverse: psi^-N/2 as (w, w/q)
+    u32 log2N;
+    double2 cinv[kMaxL];   // inverse: c_loc = psi^-(NC/2) as (w, w/q)
 };
 cudaError_t plan_ntt_c5(ephdc_ntt_plan *p);
 void ephdc_ntt_plan_c5_free(ephdc_ntt_plan *p);

@@ -736,24 +736,27 @@ size_t ntt_mac_smem_bytes(uint32_t lgc) {
 }
 
 template <int LGC, int S>
-static cudaError_t ntt_mac_launch(const ephdc_ctx *c, const u32 *M, const u64 *model, u64 *out, cudaStream_t st) {
+static cudaError_t ntt_mac_launch(const ephdc_ctx *c, const u32 *M, const u64 *model, u64 *out, cudaStream_t st,
+                                  uint32_t d_lim) {
     const size_t smem = ntt_mac_smem_bytes(LGC);
     auto kern = k_ntt_mac<LGC, S>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     const u32 grid = c->L * S * c->fused_chunks;
-    kern<<<grid, (1 << LGC) / kE, smem, st>>>(M, model, out, mac_args(c));
+    MacArgs a = mac_args(c);
+    a.D_live = std::min(a.D_live, d_lim);   // ephdc_infer_batch_prefix: the first d_lim dims
+    kern<<<grid, (1 << LGC) / kE, smem, st>>>(M, model, out, a);
     return counted(cudaGetLastError());
 }
 
 cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64_t *d_model, uint64_t *d_out,
-                           cudaStream_t st) {
+                           cudaStream_t st, uint32_t d_lim) {
     switch (c->p.log2N) {
-        case 10: return ntt_mac_launch<10, 1>(c, d_M, d_model, d_out, st);
-        case 11: return ntt_mac_launch<11, 1>(c, d_M, d_model, d_out, st);
-        case 12: return ntt_mac_launch<12, 1>(c, d_M, d_model, d_out, st);
-        case 13: return ntt_mac_launch<13, 1>(c, d_M, d_model, d_out, st);
-        case 14: return ntt_mac_launch<13, 2>(c, d_M, d_model, d_out, st);
+        case 10: return ntt_mac_launch<10, 1>(c, d_M, d_model, d_out, st, d_lim);
+        case 11: return ntt_mac_launch<11, 1>(c, d_M, d_model, d_out, st, d_lim);
+        case 12: return ntt_mac_launch<12, 1>(c, d_M, d_model, d_out, st, d_lim);
+        case 13: return ntt_mac_launch<13, 1>(c, d_M, d_model, d_out, st, d_lim);
+        case 14: return ntt_mac_launch<13, 2>(c, d_M, d_model, d_out, st, d_lim);
     }
     return cudaErrorInvalidValue;
 }

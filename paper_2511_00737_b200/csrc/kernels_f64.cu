@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(mac_threads<LGC, E>(), mac_min_blocks<LGC, E>(
     const u32 chunk = x % a.chunks, grp = x / a.chunks;
     const u32 b = grp * a.bg + bl;
     if (b >= a.nb) return;
-    const u32 d0 = chunk * a.G, d1 = min(a.D, d0 + a.G);
+    // dlim (ephdc_infer_batch_prefix): batch b sums only its first dlim[b] dims
+    const u32 d0 = chunk * a.G, d1 = min(a.dlim ? min(a.D, a.dlim[b]) : a.D, d0 + a.G);
     if (d0 >= d1) return;
 
     const u32 *Mb = M + (size_t)b * a.D * N;
@@ -652,7 +653,7 @@ template <class K> static cudaError_t smem_attr(K kernel, size_t bytes) {
 
 template <int LGC, int S>
 static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, const u32 *M, uint32_t nb,
-                                  const double *model, u64 *out, cudaStream_t st) {
+                                  const double *model, u64 *out, cudaStream_t st, const uint32_t *dlim) {
     // pad shared memory so that no more CTAs share an SM than its TMEM holds
     const size_t smem = std::max<size_t>(mac_f64_smem<LGC, S>(), (200u << 10) / f64_ctas_per_sm<LGC>());
     // Plan (profiles/r01/ab_wl2.txt): at NC = 2^13 the windowed tail (WL = 2: the last
@@ -682,6 +683,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     a.nb = nb;
     f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
     a.flags = prefetch ? 0u : 1u;  // bit 0: no explicit L2 prefetch of the model slice
+    a.dlim = dlim;
     // plan overrides (ephdc_plan bg / G; tests and profiling only)
     if (plan.bg) a.bg = std::max<u32>(1, std::min<u32>(nb, plan.bg));
     if (plan.G) {  // <= 1024 chunks: the 64-bit fold of f64_grid
@@ -698,14 +700,14 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
 
 
 cudaError_t launch_ntt_mac_f64(const ephdc_ctx *c, const ephdc_plan &plan, const uint32_t *d_M, uint32_t nb,
-                               const double *d_model, uint64_t *d_out, cudaStream_t st) {
+                               const double *d_model, uint64_t *d_out, cudaStream_t st, const uint32_t *d_dlim) {
     if (nb == 0) return cudaSuccess;
     switch (c->p.log2N) {
-        case 10: return mac_f64_launch<10, 1>(c, plan, d_M, nb, d_model, d_out, st);
-        case 11: return mac_f64_launch<11, 1>(c, plan, d_M, nb, d_model, d_out, st);
-        case 12: return mac_f64_launch<12, 1>(c, plan, d_M, nb, d_model, d_out, st);
-        case 13: return mac_f64_launch<13, 1>(c, plan, d_M, nb, d_model, d_out, st);
-        case 14: return mac_f64_launch<13, 2>(c, plan, d_M, nb, d_model, d_out, st);
+        case 10: return mac_f64_launch<10, 1>(c, plan, d_M, nb, d_model, d_out, st, d_dlim);
+        case 11: return mac_f64_launch<11, 1>(c, plan, d_M, nb, d_model, d_out, st, d_dlim);
+        case 12: return mac_f64_launch<12, 1>(c, plan, d_M, nb, d_model, d_out, st, d_dlim);
+        case 13: return mac_f64_launch<13, 1>(c, plan, d_M, nb, d_model, d_out, st, d_dlim);
+        case 14: return mac_f64_launch<13, 2>(c, plan, d_M, nb, d_model, d_out, st, d_dlim);
     }
     return cudaErrorInvalidValue;
 }

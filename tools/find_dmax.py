@@ -1,19 +1,28 @@
 #!/usr/bin/env python
-"""findDmax on the GPU (Algorithm 1 lines 17-24).
+"""findDmax on the GPU, as Algorithm 1 defines it:
 
-Algorithm 1 repeats, 1000 times, "grow D while evalHEcomputation(N, T, D+1) decrypts
-correctly" and returns the mean D_i.  Each trial here is one scores ciphertext of the
-real hot path (encode + pack + lift/NTT/MAC over D dims, `ephdc_infer_batch`) on
-synthetic queries; `ephdc_noise_probe` measures its noise exactly on the GPU.  Instead
-of re-evaluating every D (at c2-c4 the budget allows ~1e20+ dims, so the literal loop
-would not terminate -- DESIGN.md reading #21), D_i is extrapolated from the measured
-noise with the random-walk growth |e| ~ sqrt(D) that tests/test_oracle_noise.py pins
-against the closed form:  D_i = D * (Delta/2 / |e_i|)^2  (D_i = 0 when trial i already
-fails at D; that is the literal outcome at c1).  --dims evaluates several D (the
-model's first D dims) and checks the sqrt(D) growth on the GPU as well.
+    for i in range(1000):
+        D_i = 0
+        while evalHEcomputation(N, T, D_i + 1) is correct: D_i += 1
+    return average {D_i}
 
-usage: python tools/find_dmax.py [--configs c1 c1q3 c2 c3 c4] [--trials 1000] [--dims ...]
-One JSON line per (config, D).
+Trial i is one random ct x pt dot product of the real hot path: a batch of B = N/k
+plaintext query hypervectors (uniform in +-qmax, SPEC: "probe plaintexts drawn
+uniformly at max quantized magnitude") against an encrypted model of uniform class
+hypervectors; evalHEcomputation(N, T, D) sums its first D dims
+(`ephdc_infer_batch_prefix`) and is correct when the decrypted scores equal the
+plaintext dot products mod t (library decryption, `ephdc_decrypt_scores`).  The 1000
+trials run as 1000 batches of ONE call per probed D.  The first failing D of each
+trial is found by bisection between a correct and a failing D (every probed D is a
+real evaluation; a trial still correct at D_cap is reported censored).
+
+Parameters: N in {2^11, 2^12, 2^13} with Sum log2 q at the 128-bit-security caps of
+SPEC.md l.190 (54, 109, 218 bits; primes < 2^50 so the FP64 kernels run), t = the
+largest prime = 1 mod 2N below 2^T, T swept over the range where D_max is between
+~1 and D_cap (Fig. "D_max for various N and log2 t").
+
+usage: python tools/find_dmax.py [--logN 11 12 13] [--trials 1000] [--dcap 8192]
+One JSON line per (N, T).
 """
 from __future__ import annotations
 
@@ -30,59 +39,120 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+Q_BITS = {11: (27, 27), 12: (36, 36, 37), 13: (43, 43, 44, 44, 44)}   # SPEC.md l.190 caps: 54 / 109 / 218
+
+
+def predicted_dmax(N: int, t: int, Q: int) -> float:
+    """Closed form of tests/test_oracle_noise.py: noise ~ r_t(Q) sqrt(N) t/6 sqrt(D) * 2^1.5."""
+    half_delta = (Q // t) / 2
+    unit = (Q % t) * math.sqrt(N) * t / 6 * 2 ** 1.5
+    return (half_delta / unit) ** 2
+
+
+class Probe:
+    """One (N, T) point: context, key, encrypted uniform model, uniform query HVs."""
+
+    def __init__(self, logN: int, T: int, trials: int, dcap: int, k: int = 2, bits: int = 4, seed: int = 0,
+                 device: int = 0):
+        import torch
+        import ephdc_inputs as inp
+        import paper_2511_00737_b200 as eph
+        self.torch, self.eph = torch, eph
+        N = 1 << logN
+        t = eph.find_ntt_primes(logN, [T])[0]
+        q = eph.find_ntt_primes(logN, list(Q_BITS[logN]), exclude=[t])
+        self.N, self.t, self.q, self.k, self.dcap, self.trials = N, t, q, k, dcap, trials
+        self.Q = math.prod(q)
+        qmax = (1 << (bits - 1)) - 1
+        self.ctx = eph.Context(log2N=logN, q=q, t=t, k=k, D_live=dcap, D_stored=dcap, F=64, feat_unsigned=False,
+                               Qbits=bits, Cbits=bits, qshift=0, device=device)
+        assert self.ctx.arith == "f64"
+        self.B = self.ctx.B
+        self.nq = trials * self.B
+        rng = np.random.default_rng([seed, logN, T])
+        self.C = rng.integers(-qmax, qmax + 1, size=(k, dcap), dtype=np.int8)       # class HVs (host, encrypted)
+        self.sk = eph.SecretKey(self.ctx, 1000 + seed)
+        self.model = eph.EncryptedModel(self.ctx, self.sk, self.C, 2000 + seed)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(int(rng.integers(1 << 62)))
+        self.H = torch.randint(-qmax, qmax + 1, (dcap, self.nq), generator=g, device="cuda", dtype=torch.int8)
+        self.ws = eph.Workspace(self.ctx, self.nq)
+        self.Cd = torch.from_numpy(self.C.astype(np.float64)).cuda()
+
+    def expected(self, dims: np.ndarray) -> np.ndarray:
+        """Plaintext dot products of every trial's first dims[b] dims, centered mod t: [nq][k]."""
+        torch = self.torch
+        out = np.empty((self.nq, self.k), dtype=np.int64)
+        for b, D in enumerate(dims):
+            cols = slice(b * self.B, (b + 1) * self.B)
+            s = (self.Cd[:, :D] @ self.H[:D, cols].double()).T        # exact: |s| < 2^53
+            out[cols] = s.cpu().numpy().astype(np.int64)
+        t = self.t
+        return ((out + (t - 1) // 2) % t) - (t - 1) // 2
+
+    def correct(self, dims: np.ndarray) -> np.ndarray:
+        """evalHEcomputation(N, T, dims[b]) is correct, per trial b."""
+        cts = self.eph.infer_batch_prefix(self.ctx, self.model, self.ws, self.H, self.nq, dims)
+        self.torch.cuda.synchronize()
+        S, _ = self.eph.decrypt_scores(self.ctx, self.sk, cts.cpu().numpy().view(np.uint64), self.nq)
+        ok = (S == self.expected(dims)).reshape(self.trials, self.B * self.k).all(axis=1)
+        return ok
+
+    def find_dmax(self):
+        """Per trial: the largest D with every length <= D ... evaluated by bisection
+        between lo (correct) and hi (failing); returns (D_i, censored mask, #evaluations)."""
+        n = self.trials
+        lo = np.zeros(n, dtype=np.int64)                  # D = 0: nothing summed, trivially correct
+        hi = np.full(n, self.dcap + 1, dtype=np.int64)
+        top = self.correct(np.full(n, self.dcap, dtype=np.uint32))
+        lo[top] = self.dcap
+        evals = 1
+        while np.any(hi - lo > 1):
+            mid = np.where(hi - lo > 1, (lo + hi) // 2, lo)
+            ok = self.correct(mid.astype(np.uint32))
+            act = hi - lo > 1
+            lo = np.where(act & ok, mid, lo)
+            hi = np.where(act & ~ok, mid, hi)
+            evals += 1
+        return lo, top, evals
+
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", nargs="+", default=["c1", "c1q3", "c2", "c3", "c4"])
+    ap.add_argument("--logN", nargs="+", type=int, default=[11, 12, 13])
     ap.add_argument("--trials", type=int, default=1000)
-    ap.add_argument("--dims", nargs="*", type=int, default=[], help="D values (default: the config's D_live)")
+    ap.add_argument("--dcap", type=int, default=8192)
+    ap.add_argument("--Ts", nargs="*", type=int, default=[], help="log2 t values (default: the range where 1 <= D_max <= dcap)")
     a = ap.parse_args()
-    import torch
-    import ephdc_inputs as inp
     import paper_2511_00737_b200 as eph
-    from paper_2511_00737_b200 import pipeline as ppipe
 
-    for name in a.configs:
-        base = inp.CONFIGS[name]
-        for D in (a.dims or [base.D_live]):
-            if D > base.D_live:
-                continue
-            cfg = dataclasses.replace(base, D_live=D)
-            t, q = ppipe.primes_for(cfg)
-            Q = math.prod(int(x) for x in q)
-            half_delta = (Q // t) // 2
-            Xtr, ytr, _, _ = inp.gen_features(cfg, 1)
-            P = inp.gen_projection(cfg)
-            ps = ppipe.build(cfg, P, Xtr, ytr)
-            B = ps.ctx.B
-            nq = a.trials * B
-            rng = np.random.default_rng([cfg.seed, 77, D])
-            hi = 256 if cfg.feat_unsigned else 128
-            Xq = rng.integers(0 if cfg.feat_unsigned else -128, hi, size=(nq, cfg.F),
-                              dtype=np.uint8 if cfg.feat_unsigned else np.int8)
-            X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
-            ws = eph.Workspace(ps.ctx, nq)
-            torch.cuda.synchronize()
+    for logN in a.logN:
+        N = 1 << logN
+        Ts = list(a.Ts)
+        if not Ts:
+            for T in range(60, 10, -1):   # predicted D_max from 1 to dcap / 2 (plus one step on each side)
+                try:
+                    t = eph.find_ntt_primes(logN, [T])[0]
+                    q = eph.find_ntt_primes(logN, list(Q_BITS[logN]), exclude=[t])
+                except Exception:
+                    continue
+                pd = predicted_dmax(N, t, math.prod(q))
+                if pd >= 0.25 and pd <= 2 * a.dcap:
+                    Ts.append(T)
+        for T in sorted(Ts, reverse=True):
             t0 = time.perf_counter()
-            H = eph.encode_queries(ps.ctx, X, ps.P_dev)
-            cts = eph.infer_batch(ps.ctx, ps.model, ws, H, nq)
-            torch.cuda.synchronize()
+            p = Probe(logN, T, a.trials, a.dcap)
             t1 = time.perf_counter()
-            bits, flags, lg = eph.noise_probe(ps.ctx, ps.sk, cts)
+            Di, cens, evals = p.find_dmax()
             t2 = time.perf_counter()
-            hd = math.log2(half_delta)
-            fails = (lg >= hd) | (flags != 0)
-            Di = np.where(fails, 0.0, D * np.exp2(2.0 * (hd - lg)))
-            line = {"workload": name, "D": D, "trials": int(a.trials), "N": ps.ctx.N, "L": ps.ctx.L, "t": int(t),
-                    "log2_half_delta": round(hd, 3),
-                    "noise_log2_mean": round(float(lg.mean()), 3), "noise_log2_max": round(float(lg.max()), 3),
-                    "noise_bits_max": int(bits.max()), "decrypt_fail_trials": int(fails.sum()),
-                    "D_max_mean": float(Di.mean()), "D_max_min": float(Di.min()),
-                    "closed_form_noise_log2": round(math.log2((Q % t) * math.sqrt(ps.ctx.N) * t / 6 * math.sqrt(D)) + 1.5, 3),
-                    "gpu_eval_s": round(t1 - t0, 3), "gpu_probe_s": round(t2 - t1, 3)}
-            print(json.dumps(line), flush=True)
-            del cts, H, X, ws, ps
-            torch.cuda.empty_cache()
+            print(json.dumps({"N": N, "log2_t": T, "t": p.t, "q": p.q, "log2_Q": round(math.log2(p.Q), 2),
+                              "trials": a.trials, "batch_B": p.B, "D_cap": a.dcap,
+                              "D_max_mean": float(Di.mean()), "D_max_std": float(Di.std()),
+                              "D_max_min": int(Di.min()), "D_max_max": int(Di.max()),
+                              "censored_trials": int(cens.sum()), "evaluations": evals,
+                              "predicted_D_max": round(predicted_dmax(N, p.t, p.Q), 2),
+                              "setup_s": round(t1 - t0, 2), "search_s": round(t2 - t1, 2)}), flush=True)
+            del p
 
 
 if __name__ == "__main__":

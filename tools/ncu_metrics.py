@@ -58,8 +58,10 @@ def main():
                            "fmaheavy_cycles_pct": f(k["sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"]),
                            "issue_active_pct": f(k["smsp__issue_active.avg.pct_of_peak_sustained_active"])}
         elif "k_encode_tc" in name and "encode" not in out:
-            out["encode"] = {"kernel": name.split("(")[0], "duration_ms": ms,
-                             "tensor_pipe_pct": f(k["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"])}
+            # tcgen05 MMAs: the realtime tensor-pipe counter (the plain sm__pipe_tensor_cycles_active
+            # stays 0 for UTC*MMA on this ncu)
+            tp = f(k.get("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"))
+            out["encode"] = {"kernel": name.split("(")[0], "duration_ms": ms, "tensor_pipe_pct": tp}
     try:
         allm = json.load(open(path))
     except Exception:
