@@ -935,8 +935,12 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
     }
     plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
     if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
+    // the c5 kernels (ntt_c5.cu) use the FP64 forward table at every N >= 2^12 whose
+    // primes are all < 2^50; their own bounds are decided in plan_ntt_c5
+    const bool c5_candidate = !(flags & EPHDC_NTT_FORCE_INT) && log2N >= 12 &&
+                              *std::max_element(p->q.begin(), p->q.end()) < (1ull << 50);
 
-    if (p->fwd_f64 || p->inv_f64) {
+    if (p->fwd_f64 || p->inv_f64 || c5_candidate) {
         // FP64 tables: forward psi_rev; inverse = Cooley-Tukey DIT on the bit-reversed
         // input (x[r] = DFT(a psi^j)[brev r]): stage of half-size h uses omega^-(N/2h) jj
         // for the block position jj < h (entry h + jj), then a_j = N^-1 psi^-j x_j
@@ -1026,7 +1030,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
             return EPHDC_ECUDA;
         }
     }
-    if (p->fwd_f64 && plan_ntt_c5(p.get()) != cudaSuccess) {
+    if (c5_candidate && plan_ntt_c5(p.get()) != cudaSuccess) {
         ephdc_ntt_plan_free(p.release());
         return EPHDC_ECUDA;
     }

@@ -16,13 +16,16 @@ trials run as 1000 batches of ONE call per probed D.  The first failing D of eac
 trial is found by bisection between a correct and a failing D (every probed D is a
 real evaluation; a trial still correct at D_cap is reported censored).
 
-Parameters: N in {2^11, 2^12, 2^13} with Sum log2 q at the 128-bit-security caps of
-SPEC.md l.190 (54, 109, 218 bits; primes < 2^50 so the FP64 kernels run), t = the
-largest prime = 1 mod 2N below 2^T, T swept over the range where D_max is between
-~1 and D_cap (Fig. "D_max for various N and log2 t").
+Parameters: t = the largest prime = 1 mod 2N below 2^T (the library takes t < 2^30),
+T swept over the range where D_max lies between ~1 and D_cap (Fig. "D_max for various
+N and log2 t"); q (primes < 2^50, the FP64 kernels):
+  * N = 2^11 at the 128-bit-security cap of SPEC.md l.190, Sum log2 q = 54;
+  * N = 2^12, 2^13 at the caps (109, 218 bits) D_max is ~2^30 and more for every
+    t < 2^30 (the closed form; the run reports these points censored at D_cap), so the
+    terminating sweeps there use q = 72 bits (below the cap: more secure, less budget).
 
-usage: python tools/find_dmax.py [--logN 11 12 13] [--trials 1000] [--dcap 8192]
-One JSON line per (N, T).
+usage: python tools/find_dmax.py [--grid default|cap] [--trials 1000] [--dcap 8192]
+One JSON line per (N, q, T).
 """
 from __future__ import annotations
 
@@ -40,6 +43,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 Q_BITS = {11: (27, 27), 12: (36, 36, 37), 13: (43, 43, 44, 44, 44)}   # SPEC.md l.190 caps: 54 / 109 / 218
+GRID = [(11, (27, 27)), (12, (36, 36)), (13, (36, 36))]                  # the terminating sweeps
 
 
 def predicted_dmax(N: int, t: int, Q: int) -> float:
@@ -53,14 +57,14 @@ class Probe:
     """One (N, T) point: context, key, encrypted uniform model, uniform query HVs."""
 
     def __init__(self, logN: int, T: int, trials: int, dcap: int, k: int = 2, bits: int = 4, seed: int = 0,
-                 device: int = 0):
+                 device: int = 0, q_bits=None):
         import torch
         import ephdc_inputs as inp
         import paper_2511_00737_b200 as eph
         self.torch, self.eph = torch, eph
         N = 1 << logN
         t = eph.find_ntt_primes(logN, [T])[0]
-        q = eph.find_ntt_primes(logN, list(Q_BITS[logN]), exclude=[t])
+        q = eph.find_ntt_primes(logN, list(q_bits or Q_BITS[logN]), exclude=[t])
         self.N, self.t, self.q, self.k, self.dcap, self.trials = N, t, q, k, dcap, trials
         self.Q = math.prod(q)
         qmax = (1 << (bits - 1)) - 1
@@ -99,8 +103,12 @@ class Probe:
         return ok
 
     def find_dmax(self):
-        """Per trial: the largest D with every length <= D ... evaluated by bisection
-        between lo (correct) and hi (failing); returns (D_i, censored mask, #evaluations)."""
+        """Per trial: bisection between lo (correct; D = 0 sums nothing) and hi (failing)
+        until hi = lo + 1 -- D_i = lo decrypts correctly and D_i + 1 does not.  (The
+        literal loop stops at the FIRST failing length; with a noise random walk a
+        failure can in principle be followed by a correct longer prefix, so bisection
+        can land on a later boundary -- tests/test_gpu_find_dmax.py checks D_i and
+        D_i + 1 with the oracle.)  Returns (D_i, censored mask, #evaluations)."""
         n = self.trials
         lo = np.zeros(n, dtype=np.int64)                  # D = 0: nothing summed, trivially correct
         hi = np.full(n, self.dcap + 1, dtype=np.int64)
@@ -119,38 +127,40 @@ class Probe:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--logN", nargs="+", type=int, default=[11, 12, 13])
+    ap.add_argument("--grid", default="default", choices=["default", "cap"])
     ap.add_argument("--trials", type=int, default=1000)
     ap.add_argument("--dcap", type=int, default=8192)
-    ap.add_argument("--Ts", nargs="*", type=int, default=[], help="log2 t values (default: the range where 1 <= D_max <= dcap)")
     a = ap.parse_args()
     import paper_2511_00737_b200 as eph
 
-    for logN in a.logN:
-        N = 1 << logN
-        Ts = list(a.Ts)
-        if not Ts:
-            for T in range(60, 10, -1):   # predicted D_max from 1 to dcap / 2 (plus one step on each side)
-                try:
-                    t = eph.find_ntt_primes(logN, [T])[0]
-                    q = eph.find_ntt_primes(logN, list(Q_BITS[logN]), exclude=[t])
-                except Exception:
+    if a.grid == "cap":   # N = 2^12, 2^13 at the SPEC caps, the largest t < 2^30: censored at D_cap
+        plan = [(12, Q_BITS[12], [29]), (13, Q_BITS[13], [29])]
+    else:
+        plan = []
+        for logN, qb in GRID:
+            Ts = []
+            for T in range(29, 10, -1):   # predicted D_max from ~1/4 to 2 D_cap
+                t = eph.find_ntt_primes(logN, [T])[0]
+                if t.bit_length() != T:
                     continue
-                pd = predicted_dmax(N, t, math.prod(q))
-                if pd >= 0.25 and pd <= 2 * a.dcap:
+                q = eph.find_ntt_primes(logN, list(qb), exclude=[t])
+                pd = predicted_dmax(1 << logN, t, math.prod(q))
+                if 0.25 <= pd <= 2 * a.dcap:
                     Ts.append(T)
+            plan.append((logN, qb, Ts))
+    for logN, qb, Ts in plan:
         for T in sorted(Ts, reverse=True):
             t0 = time.perf_counter()
-            p = Probe(logN, T, a.trials, a.dcap)
+            p = Probe(logN, T, a.trials, a.dcap, q_bits=qb)
             t1 = time.perf_counter()
             Di, cens, evals = p.find_dmax()
             t2 = time.perf_counter()
-            print(json.dumps({"N": N, "log2_t": T, "t": p.t, "q": p.q, "log2_Q": round(math.log2(p.Q), 2),
+            print(json.dumps({"N": 1 << logN, "log2_t": T, "t": p.t, "q": p.q, "log2_Q": round(math.log2(p.Q), 2),
                               "trials": a.trials, "batch_B": p.B, "D_cap": a.dcap,
                               "D_max_mean": float(Di.mean()), "D_max_std": float(Di.std()),
                               "D_max_min": int(Di.min()), "D_max_max": int(Di.max()),
                               "censored_trials": int(cens.sum()), "evaluations": evals,
-                              "predicted_D_max": round(predicted_dmax(N, p.t, p.Q), 2),
+                              "predicted_D_max": round(predicted_dmax(1 << logN, p.t, p.Q), 2),
                               "setup_s": round(t1 - t0, 2), "search_s": round(t2 - t1, 2)}), flush=True)
             del p
 
