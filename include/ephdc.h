@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define EPHDC_ABI_VERSION 2
+#define EPHDC_ABI_VERSION 3
 #define EPHDC_MAX_PRIMES 16
 
 typedef enum {
@@ -125,6 +125,27 @@ typedef struct ephdc_model ephdc_model;
 typedef struct ephdc_workspace ephdc_workspace;
 typedef struct ephdc_ntt_plan ephdc_ntt_plan;
 
+/* Key of the random streams (reading #7): every secret-key coefficient, uniform a and
+ * Gaussian e is a 64-bit word of a ChaCha20 block (RFC 8439 sec. 2.3) under this
+ * 256-bit key, the block counter and nonce naming the value (tag, ciphertext index,
+ * coefficient).  Threat model: c1 = a is published to the client, so the
+ * generator must be a PRF under a key the client cannot guess -- a NULL seed pointer
+ * (every entry point below that takes one) draws a fresh key from the OS CSPRNG.
+ * Callers that need reproducible streams (parity tests, benchmarks) build a key with
+ * ephdc_seed_u64: deterministic and GUESSABLE, never for real data. */
+typedef struct {
+    uint32_t key[8];
+} ephdc_seed;
+/* key <- 32 bytes of getrandom(2).  Errors: ENULL, ERESOURCE (no OS entropy). */
+ephdc_status ephdc_seed_os(ephdc_seed *out);
+/* TEST/BENCH ONLY: key = (lo32(v), hi32(v), 0, 0, 0, 0, 0, 0).  Errors: ENULL. */
+ephdc_status ephdc_seed_u64(uint64_t v, ephdc_seed *out);
+/* One ChaCha20 block (RFC 8439 sec. 2.3.1) of the library's generator, host side:
+ * out[16] words for (key, counter, nonce[3]) -- exported so tests can pin it to the
+ * RFC's known answers.  Errors: ENULL. */
+ephdc_status ephdc_chacha20_block(const ephdc_seed *key, uint32_t counter, const uint32_t nonce[3],
+                                  uint32_t out[16]);
+
 const char *ephdc_status_string(ephdc_status s);
 int ephdc_abi_version(void);
 
@@ -178,9 +199,10 @@ ephdc_status ephdc_ctx_query(const ephdc_ctx *ctx, ephdc_ctx_info *info);
 
 /* ---------------- server side (CS1) ---------------------------- */
 
-/* Secret key: ternary s (reading #9) from SplitMix64 stream (seed, 2,
- * 0, i) (reading #7), and s_hat_j = NTT_j(s).  Host-only, deterministic. */
-ephdc_status ephdc_keygen(const ephdc_ctx *ctx, uint64_t seed, ephdc_sk **out);
+/* Secret key: ternary s (reading #9) from the ChaCha20 stream of tag 2
+ * (reading #7) under `seed` (NULL: a fresh OS key), and s_hat_j = NTT_j(s).
+ * Host-only.  Errors: ENULL, ERESOURCE. */
+ephdc_status ephdc_keygen(const ephdc_ctx *ctx, const ephdc_seed *seed, ephdc_sk **out);
 void ephdc_sk_free(ephdc_sk *sk);
 /* s_out[N] int8 in {-1,0,1}; s_hat_out[L][N] (may be NULL). */
 ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_out);
@@ -189,11 +211,12 @@ ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_
  * d < D_live, m_d = encode(tile_d), tile_d[i] = class_hv[i mod k][d] mod t for
  * i < k*B else 0; per prime: c1 = a (uniform in the NTT domain, #6, #8),
  * c0 = NTT_j([Delta*m_d + e_d]_{q_j}) - a (.) s_hat_j (secret-key BFV, #4, #5;
- * e_d CDT Gaussian, #10).  class_hv: HOST int8 [k][D_live] with |v| < t/2.
- * The model lives on the context's device: u64 [D_live][L][2][N].
+ * e_d CDT Gaussian, #10); a and e from the ChaCha20 streams of ciphertext index d
+ * under `seed` (NULL: a fresh OS key, independent of the secret key's).
+ * class_hv: HOST int8 [k][D_live] with |v| < t/2.  The model lives on the context's device: u64 [D_live][L][2][N].
  * Synchronous.  Errors: ENULL, ECONTEXT (host-only ctx), ECUDA, ERESOURCE. */
 ephdc_status ephdc_encrypt_model(const ephdc_ctx *ctx, const ephdc_sk *sk, const int8_t *class_hv,
-                                 uint64_t seed, ephdc_model **out);
+                                 const ephdc_seed *seed, ephdc_model **out);
 void ephdc_model_free(ephdc_model *m);
 /* Copies ciphertexts of dims [d0, d0+nd) to host_out [nd][L][2][N] (canonical).
  * Synchronous.  EPARAM if d0+nd > D_live. */
@@ -291,10 +314,11 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *ctx, const ephdc_model *model,
 
 /* Client: batch b of d_H [D_live][nq] -> d_qct [D_live][L][2][N]: secret-key BFV with
  * the client's key (readings #4-#10), random streams of ciphertext index 2^32 + b*D_live + d (#25: disjoint from the model's
- * indices d < D_live, so query and model ciphertexts never share a or e).
- * Uses the workspace's plaintext buffer.  Async. */
+ * indices d < D_live, so query and model ciphertexts never share a or e) under `seed`
+ * (NULL: a fresh OS key per call).  Uses the workspace's plaintext buffer.  Async. */
 ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *ctx, ephdc_sk *sk, ephdc_workspace *ws, const int8_t *d_H,
-                                      uint32_t nq, uint32_t b, uint64_t seed, uint64_t *d_qct, void *stream);
+                                      uint32_t nq, uint32_t b, const ephdc_seed *seed, uint64_t *d_qct,
+                                      void *stream);
 /* Server, once: the plaintext class tiles in NTT form, d_pt [D_live][L][N] canonical:
  * NTT_j(centered lift(encode(tile_d))).  h_class_hv: HOST int8 [k][D_live].  Synchronous. */
 ephdc_status ephdc_sr_model_plaintexts(const ephdc_ctx *ctx, const int8_t *h_class_hv, uint64_t *d_pt);

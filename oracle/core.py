@@ -52,9 +52,8 @@ def lib() -> ctypes.CDLL:
             "or_ntt_inv_many": (None, [P, u64, ctypes.c_int, u64, u64]),
             "or_eval": (u64, [P, u32, u64, u64]),
             "or_negacyclic_mul": (None, [P, P, P, u32, u64]),
-            "or_mix64": (u64, [u64]),
-            "or_stream": (u64, [u64, u64, u64, u64]),
-            "or_draw": (u64, [u64, u64]),
+            "or_chacha20_block": (None, [P, u32, P, P]),
+            "or_word64": (u64, [u64, u32, u64, u32, u32]),
             "or_sample_ternary": (None, [u64, u32, P]),
             "or_uniform_mod": (u64, [u64, u64, u32, u32, u32, u64]),
             "or_gauss": (ctypes.c_longlong, [u64, u64, u32, P, ctypes.c_int]),

@@ -17,7 +17,7 @@
  *                      ("encrypted ... using a given secret key"; readings #4-#6)
  *   - client eval    : acc_j = sum_d c_{d,j} (.) NTT_j(lift_j(encode(v_{b,d})))
  *                      (D MulCP, D-1 AddCC, 0 Rot)
- *   - randomness     : SplitMix64 streams of DESIGN.md reading #7-#11.
+ *   - randomness     : ChaCha20 (RFC 8439) streams of DESIGN.md readings #7-#10.
  * OpenMP only splits independent dims d across threads; each thread runs the
  * same plain loop and the per-thread sums are added mod q at the end.
  */
@@ -143,27 +143,53 @@ void or_negacyclic_mul(const u64 *a, const u64 *b, u64 *c, u32 N, u64 q) {
 }
 
 /* ------------------------------------------------------------------ */
-/* randomness: SplitMix64 streams (reading #7)               */
+/* randomness: ChaCha20 streams (reading #7)                 */
 /* ------------------------------------------------------------------ */
-#define GOLD 0x9E3779B97F4A7C15ULL
-u64 or_mix64(u64 z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
+/* RFC 8439 sec. 2.1: the quarter round on four words of the state */
+#define ROTL32(v, n) (((v) << (n)) | ((v) >> (32 - (n))))
+static void quarter_round(u32 *s, int a, int b, int c, int d) {
+    s[a] += s[b]; s[d] ^= s[a]; s[d] = ROTL32(s[d], 16);
+    s[c] += s[d]; s[b] ^= s[c]; s[b] = ROTL32(s[b], 12);
+    s[a] += s[b]; s[d] ^= s[a]; s[d] = ROTL32(s[d], 8);
+    s[c] += s[d]; s[b] ^= s[c]; s[b] = ROTL32(s[b], 7);
 }
-u64 or_stream(u64 seed, u64 tag, u64 a, u64 b) {
-    u64 h = or_mix64(seed ^ (tag * GOLD));
-    h = or_mix64(h ^ (a * 0xD1B54A32D192ED03ULL));
-    return or_mix64(h ^ (b * 0x8CB92BA72F3D8DD7ULL));
+/* RFC 8439 sec. 2.3: state = constants | key[8] | counter | nonce[3];
+   10 x (4 column rounds + 4 diagonal rounds); out = state + working state */
+void or_chacha20_block(const u32 *key, u32 counter, const u32 *nonce, u32 *out) {
+    u32 st[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
+                  key[0], key[1], key[2], key[3], key[4], key[5], key[6], key[7],
+                  counter, nonce[0], nonce[1], nonce[2]};
+    u32 w[16];
+    memcpy(w, st, sizeof w);
+    for (int r = 0; r < 10; ++r) {
+        quarter_round(w, 0, 4, 8, 12);
+        quarter_round(w, 1, 5, 9, 13);
+        quarter_round(w, 2, 6, 10, 14);
+        quarter_round(w, 3, 7, 11, 15);
+        quarter_round(w, 0, 5, 10, 15);
+        quarter_round(w, 1, 6, 11, 12);
+        quarter_round(w, 2, 7, 8, 13);
+        quarter_round(w, 3, 4, 9, 14);
+    }
+    for (int i = 0; i < 16; ++i) out[i] = w[i] + st[i];
 }
-/* n-th output of SplitMix64 whose state starts at st */
-u64 or_draw(u64 st, u64 n) { return or_mix64(st + (n + 1) * GOLD); }
 
-enum { TAG_SK = 2, TAG_A = 3, TAG_E = 4, TAG_RES = 6 };
+enum { TAG_SK = 2, TAG_A = 3, TAG_E = 4, TAG_A_RETRY = 5 };
 
-/* reading #9: s_i = (next() mod 3) - 1 */
+/* the generator's 64-bit word w (< 8) of block `ctr` of stream (tag, a) under the test
+   key of a 64-bit seed: key = (lo32(seed), hi32(seed), 0, ..., 0), nonce = (tag,
+   lo32(a), hi32(a)); word w = block bytes 8w..8w+7 little-endian */
+u64 or_word64(u64 seed, u32 tag, u64 a, u32 ctr, u32 w) {
+    u32 key[8] = {(u32)seed, (u32)(seed >> 32), 0, 0, 0, 0, 0, 0};
+    u32 nonce[3] = {tag, (u32)a, (u32)(a >> 32)};
+    u32 b[16];
+    or_chacha20_block(key, ctr, nonce, b);
+    return (u64)b[2 * w] | ((u64)b[2 * w + 1] << 32);
+}
+
+/* reading #9: s_i = (word i%8 of block i/8 of tag 2) mod 3 - 1 */
 void or_sample_ternary(u64 seed, u32 N, int8_t *s) {
-    for (u32 i = 0; i < N; ++i) s[i] = (int8_t)((int)(or_draw(or_stream(seed, TAG_SK, 0, i), 0) % 3) - 1);
+    for (u32 i = 0; i < N; ++i) s[i] = (int8_t)((int)(or_word64(seed, TAG_SK, 0, i / 8, i % 8) % 3) - 1);
 }
 
 static u64 bitmask_for(u64 q) {
@@ -171,30 +197,54 @@ static u64 bitmask_for(u64 q) {
     while (m < q) m = (m << 1) | 1;   /* 2^ceil(log2 q) - 1 (q is never a power of two) */
     return m;
 }
-/* reading #8: uniform mod q by rejection; stream index (d*L + j, i) */
+/* reading #8: uniform mod q by rejection.  Draw 0 of coefficient i: word i%8 of block i/8
+   of stream (tag 3, d*L + j); draw n >= 1: word (n-1)%8 of block i + ((n-1)/8)*2^16 of
+   stream (tag 5, d*L + j)  (N <= 2^16) */
 u64 or_uniform_mod(u64 seed, u64 d, u32 j, u32 L, u32 i, u64 q) {
-    u64 st = or_stream(seed, TAG_A, d * L + j, i);
+    u64 a = d * L + j;
     u64 mask = bitmask_for(q);
-    for (u64 n = 0;; ++n) {
-        u64 u = or_draw(st, n) & mask;
-        if (u < q) return u;
-    }
+    u64 u = or_word64(seed, TAG_A, a, i / 8, i % 8) & mask;
+    for (u32 n = 1; u >= q; ++n) u = or_word64(seed, TAG_A_RETRY, a, i + ((n - 1) / 8) * 65536u, (n - 1) % 8) & mask;
+    return u;
 }
-/* reading #10: CDT over magnitudes, sign from a second draw */
+/* reading #10: CDT over magnitudes; block i/4 of stream (tag 4, d): magnitude from
+   word 2(i%4) >> 1, sign = top bit of word 2(i%4)+1 */
 long long or_gauss(u64 seed, u64 d, u32 i, const u64 *cdt, int ncdt) {
-    u64 st = or_stream(seed, TAG_E, d, i);
-    u64 u = or_draw(st, 0) >> 1;
+    u64 u = or_word64(seed, TAG_E, d, i / 4, 2 * (i % 4)) >> 1;
     int k = 0;
     while (k < ncdt - 1 && u >= cdt[k]) ++k;
     if (k == 0) return 0;
-    return (or_draw(st, 1) >> 63) ? -(long long)k : (long long)k;
+    return (or_word64(seed, TAG_E, d, i / 4, 2 * (i % 4) + 1) >> 63) ? -(long long)k : (long long)k;
 }
 
+/* whole polynomials: the same values as or_uniform_mod / or_gauss coefficient by
+   coefficient, each block computed once for the 8 (uniform) or 4 (Gaussian)
+   coefficients that read it (tests check the two forms agree) */
 void or_sample_uniform_poly(u64 seed, u64 d, u32 j, u32 L, u64 q, u32 N, u64 *out) {
-    for (u32 i = 0; i < N; ++i) out[i] = or_uniform_mod(seed, d, j, L, i, q);
+    u64 a = d * L + j;
+    u64 mask = bitmask_for(q);
+    u32 key[8] = {(u32)seed, (u32)(seed >> 32), 0, 0, 0, 0, 0, 0};
+    u32 nonce[3] = {TAG_A, (u32)a, (u32)(a >> 32)};
+    u32 b[16];
+    for (u32 i = 0; i < N; ++i) {
+        if (i % 8 == 0) or_chacha20_block(key, i / 8, nonce, b);
+        u64 u = ((u64)b[2 * (i % 8)] | ((u64)b[2 * (i % 8) + 1] << 32)) & mask;
+        for (u32 n = 1; u >= q; ++n) u = or_word64(seed, TAG_A_RETRY, a, i + ((n - 1) / 8) * 65536u, (n - 1) % 8) & mask;
+        out[i] = u;
+    }
 }
 void or_sample_gauss_poly(u64 seed, u64 d, u32 N, const u64 *cdt, int ncdt, long long *e) {
-    for (u32 i = 0; i < N; ++i) e[i] = or_gauss(seed, d, i, cdt, ncdt);
+    u32 key[8] = {(u32)seed, (u32)(seed >> 32), 0, 0, 0, 0, 0, 0};
+    u32 nonce[3] = {TAG_E, (u32)d, (u32)(d >> 32)};
+    u32 b[16];
+    for (u32 i = 0; i < N; ++i) {
+        if (i % 4 == 0) or_chacha20_block(key, i / 4, nonce, b);
+        u32 w = 2 * (i % 4);
+        u64 u = ((u64)b[2 * w] | ((u64)b[2 * w + 1] << 32)) >> 1;
+        int k = 0;
+        while (k < ncdt - 1 && u >= cdt[k]) ++k;
+        e[i] = k == 0 ? 0 : ((b[2 * w + 3] >> 31) ? -(long long)k : (long long)k);
+    }
 }
 
 /* ------------------------------------------------------------------ */
@@ -260,11 +310,8 @@ static void encrypt_msg(const or_bfv *P, u64 g, const u64 *m, u64 *const *psi_ta
         or_ntt_fwd(x, P->logN, q, psi_tabs[j]);
         u64 *c0 = out + ((u64)j * 2 + 0) * N;
         u64 *c1 = out + ((u64)j * 2 + 1) * N;
-        for (u32 i = 0; i < N; ++i) {
-            u64 a = or_uniform_mod(P->enc_seed, d, j, P->L, i, q);
-            c1[i] = a;
-            c0[i] = or_submod(x[i], or_mulmod(a, P->s_hat[(u64)j * N + i], q), q);
-        }
+        or_sample_uniform_poly(P->enc_seed, d, j, P->L, q, N, c1);   /* c1 = a */
+        for (u32 i = 0; i < N; ++i) c0[i] = or_submod(x[i], or_mulmod(c1[i], P->s_hat[(u64)j * N + i], q), q);
     }
 }
 

@@ -17,7 +17,7 @@ from . import _capi
 from ._capi import EphdcError, call, lib
 
 __all__ = [
-    "Context", "SecretKey", "EncryptedModel", "Workspace", "NttPlan", "EphdcError",
+    "Context", "SecretKey", "EncryptedModel", "Workspace", "NttPlan", "EphdcError", "make_seed", "chacha20_block",
     "find_ntt_primes", "min_psi", "gaussian_cdt", "query_bits", "train_model", "launch_count",
     "encode_queries", "encode_raw", "infer_batch", "infer_batch_prefix", "encode_plaintexts", "classify_host",
     "scores_message_bytes", "pack_scores", "unpack_scores", "classify_host_packed",
@@ -137,11 +137,39 @@ class Context:
             pass
 
 
+def make_seed(seed=None):
+    """ephdc_seed for the random streams (reading #7).  None: NULL, the library draws a
+    fresh 256-bit key from the OS (the default; streams nobody can reproduce); int:
+    ephdc_seed_u64 -- DETERMINISTIC and guessable, for parity tests and benchmarks only;
+    bytes (32): that key."""
+    if seed is None:
+        return None
+    s = _capi.Seed()
+    if isinstance(seed, (bytes, bytearray)):
+        if len(seed) != 32:
+            raise ValueError("a key seed is 32 bytes")
+        ctypes.memmove(s.key, bytes(seed), 32)
+    else:
+        call("ephdc_seed_u64", int(seed), ctypes.byref(s))
+    return ctypes.byref(s)
+
+
+def chacha20_block(key: bytes, counter: int, nonce) -> np.ndarray:
+    """ephdc_chacha20_block: the generator's block function (RFC 8439 sec. 2.3.1), host side."""
+    s = _capi.Seed()
+    ctypes.memmove(s.key, bytes(key), 32)
+    n = np.ascontiguousarray(nonce, dtype=np.uint32)
+    out = np.zeros(16, dtype=np.uint32)
+    call("ephdc_chacha20_block", ctypes.byref(s), counter, _np_ptr(n), _np_ptr(out))
+    return out
+
+
 class SecretKey:
-    def __init__(self, ctx: Context, seed: int):
+    def __init__(self, ctx: Context, seed=None):
+        """seed: see make_seed (None = OS entropy)."""
         self.ctx = ctx
         self._h = ctypes.c_void_p()
-        call("ephdc_keygen", ctx.handle, seed, ctypes.byref(self._h))
+        call("ephdc_keygen", ctx.handle, make_seed(seed), ctypes.byref(self._h))
 
     @property
     def handle(self):
@@ -164,13 +192,13 @@ class SecretKey:
 class EncryptedModel:
     """ephdc_model: D_live NTT-form ciphertexts resident on the device."""
 
-    def __init__(self, ctx: Context, sk: SecretKey, class_hv: np.ndarray, seed: int):
+    def __init__(self, ctx: Context, sk: SecretKey, class_hv: np.ndarray, seed=None):
         C = np.ascontiguousarray(class_hv, dtype=np.int8)
         if C.shape != (ctx.k, ctx.D_live):
             raise ValueError(f"class_hv must be [k, D_live] = {(ctx.k, ctx.D_live)}")
         self.ctx = ctx
         self._h = ctypes.c_void_p()
-        call("ephdc_encrypt_model", ctx.handle, sk.handle, _np_ptr(C), seed, ctypes.byref(self._h))
+        call("ephdc_encrypt_model", ctx.handle, sk.handle, _np_ptr(C), make_seed(seed), ctypes.byref(self._h))
 
     @property
     def handle(self):
@@ -301,13 +329,13 @@ def classify_host(ctx: Context, model: EncryptedModel, ws: Workspace, X_host, P,
 
 
 # --------------------------------------------------------------------------- HE-HDC-SR baseline
-def sr_encrypt_queries(ctx: Context, sk: SecretKey, ws: Workspace, H, nq: int, b: int, seed: int, out=None,
+def sr_encrypt_queries(ctx: Context, sk: SecretKey, ws: Workspace, H, nq: int, b: int, seed=None, out=None,
                        stream=None):
     """Client of HE-HDC-SR: batch b of H cuda [D_live, nq] -> cuda [D_live, L, 2, N] ciphertexts."""
     import torch
     if out is None:
         out = torch.empty((ctx.D_live, ctx.L, 2, ctx.N), dtype=torch.int64, device=H.device)
-    call("ephdc_sr_encrypt_queries", ctx.handle, sk.handle, ws.handle, _dptr(H), nq, b, seed, _dptr(out),
+    call("ephdc_sr_encrypt_queries", ctx.handle, sk.handle, ws.handle, _dptr(H), nq, b, make_seed(seed), _dptr(out),
          _stream(stream))
     return out
 

@@ -39,6 +39,11 @@ class Params(ctypes.Structure):
 ARITH_AUTO, ARITH_INT, ARITH_F64 = 0, 1, 2
 
 
+class Seed(ctypes.Structure):
+    """ephdc_seed: 256-bit ChaCha20 key of the random streams (reading #7)."""
+    _fields_ = [("key", c_u32 * 8)]
+
+
 class Plan(ctypes.Structure):
     _fields_ = [("flags", c_u32), ("bg", c_u32), ("G", c_u32), ("m_batches", c_u32)]
 
@@ -65,10 +70,13 @@ _SIGS = {
     "ephdc_ctx_create": (c_st, [ctypes.POINTER(Params), c_int, c_vp]),
     "ephdc_ctx_free": (None, [c_vp]),
     "ephdc_ctx_query": (c_st, [c_vp, ctypes.POINTER(CtxInfo)]),
-    "ephdc_keygen": (c_st, [c_vp, c_u64, c_vp]),
+    "ephdc_seed_os": (c_st, [ctypes.POINTER(Seed)]),
+    "ephdc_seed_u64": (c_st, [c_u64, ctypes.POINTER(Seed)]),
+    "ephdc_chacha20_block": (c_st, [ctypes.POINTER(Seed), c_u32, c_vp, c_vp]),
+    "ephdc_keygen": (c_st, [c_vp, ctypes.POINTER(Seed), c_vp]),
     "ephdc_sk_free": (None, [c_vp]),
     "ephdc_sk_export": (c_st, [c_vp, c_vp, c_vp]),
-    "ephdc_encrypt_model": (c_st, [c_vp, c_vp, c_vp, c_u64, c_vp]),
+    "ephdc_encrypt_model": (c_st, [c_vp, c_vp, c_vp, ctypes.POINTER(Seed), c_vp]),
     "ephdc_model_free": (None, [c_vp]),
     "ephdc_model_export": (c_st, [c_vp, c_u32, c_u32, c_vp]),
     "ephdc_model_scale": (c_st, [c_vp, c_vp, c_u32, c_vp, c_u32]),
@@ -83,7 +91,7 @@ _SIGS = {
     "ephdc_encode_plaintexts": (c_st, [c_vp, c_vp, c_vp, c_u32, c_u32, c_u32, c_u32, c_vp, c_vp]),
     "ephdc_classify_host": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u32, c_vp, c_u32, c_vp]),
     "ephdc_decrypt_scores": (c_st, [c_vp, c_vp, c_vp, c_u32, c_vp, c_vp]),
-    "ephdc_sr_encrypt_queries": (c_st, [c_vp, c_vp, c_vp, c_vp, c_u32, c_u32, c_u64, c_vp, c_vp]),
+    "ephdc_sr_encrypt_queries": (c_st, [c_vp, c_vp, c_vp, c_vp, c_u32, c_u32, ctypes.POINTER(Seed), c_vp, c_vp]),
     "ephdc_sr_model_plaintexts": (c_st, [c_vp, c_vp, c_vp]),
     "ephdc_sr_evaluate": (c_st, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ephdc_scores_message_bytes": (ctypes.c_size_t, [c_vp, c_u32]),

@@ -1,6 +1,7 @@
 // api.cu -- implementation of the C ABI declared in include/ephdc.h.
 #include <cuda_runtime.h>
 #include <string.h>
+#include <sys/random.h>
 #include <cstdlib>
 
 #include <algorithm>
@@ -111,6 +112,50 @@ const char *ephdc_status_string(ephdc_status s) {
 }
 
 int ephdc_abi_version(void) { return EPHDC_ABI_VERSION; }
+
+// ------------------------------------------------------------------------------------
+// random-stream keys (reading #7)
+// ------------------------------------------------------------------------------------
+ephdc_status ephdc_seed_os(ephdc_seed *out) {
+    if (!out) return EPHDC_ENULL;
+    unsigned char *p = reinterpret_cast<unsigned char *>(out->key);
+    size_t got = 0;
+    while (got < sizeof out->key) {
+        const ssize_t r = getrandom(p + got, sizeof out->key - got, 0);
+        if (r < 0) return EPHDC_ERESOURCE;
+        got += (size_t)r;
+    }
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_seed_u64(uint64_t v, ephdc_seed *out) {
+    if (!out) return EPHDC_ENULL;
+    memset(out, 0, sizeof *out);
+    out->key[0] = (uint32_t)v;
+    out->key[1] = (uint32_t)(v >> 32);
+    return EPHDC_OK;
+}
+
+ephdc_status ephdc_chacha20_block(const ephdc_seed *key, uint32_t counter, const uint32_t nonce[3], uint32_t out[16]) {
+    if (!key || !nonce || !out) return EPHDC_ENULL;
+    ephdc_rng::Key k;
+    memcpy(k.k, key->key, sizeof k.k);
+    uint32_t b[16];
+    ephdc_rng::chacha20_block(k, counter, nonce[0], nonce[1], nonce[2], b);
+    memcpy(out, b, sizeof b);
+    return EPHDC_OK;
+}
+
+namespace {
+// NULL -> a fresh OS key (the default: streams the client cannot reproduce)
+ephdc_status resolve_seed(const ephdc_seed *in, ephdc_seed *key) {
+    if (in) {
+        *key = *in;
+        return EPHDC_OK;
+    }
+    return ephdc_seed_os(key);
+}
+}  // namespace
 
 ephdc_status ephdc_query_bits(uint32_t D_live, uint32_t Cbits, uint64_t t, uint32_t *Qbits) {
     if (!Qbits) return EPHDC_ENULL;
@@ -341,14 +386,18 @@ ephdc_status ephdc_ctx_query(const ephdc_ctx *c, ephdc_ctx_info *info) {
 // ------------------------------------------------------------------------------------
 // keys and model
 // ------------------------------------------------------------------------------------
-ephdc_status ephdc_keygen(const ephdc_ctx *c, uint64_t seed, ephdc_sk **out) {
+ephdc_status ephdc_keygen(const ephdc_ctx *c, const ephdc_seed *seed, ephdc_sk **out) {
     if (!c || !out) return EPHDC_ENULL;
+    ephdc_seed key;
+    if (ephdc_status e = resolve_seed(seed, &key)) return e;
+    ephdc_rng::Key rk;
+    memcpy(rk.k, key.key, sizeof rk.k);
     std::unique_ptr<ephdc_sk> sk(new (std::nothrow) ephdc_sk());
     if (!sk) return EPHDC_ERESOURCE;
     sk->ctx = c;
     const uint32_t N = c->N;
     sk->s.resize(N);
-    for (uint32_t i = 0; i < N; ++i) sk->s[i] = (int8_t)ephdc_rng::ternary(seed, i);
+    for (uint32_t i = 0; i < N; ++i) sk->s[i] = (int8_t)ephdc_rng::ternary(rk, i);
     sk->s_hat.resize((size_t)c->L * N);
     for (uint32_t j = 0; j < c->L; ++j) {
         uint64_t *sh = sk->s_hat.data() + (size_t)j * N;
@@ -388,10 +437,12 @@ ephdc_status ephdc_sk_export(const ephdc_sk *sk, int8_t *s_out, uint64_t *s_hat_
 
 void ephdc_model_free(ephdc_model *m) { delete m; }   // ~ephdc_model frees d_ct
 
-ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const int8_t *class_hv, uint64_t seed,
-                                 ephdc_model **out) {
+ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const int8_t *class_hv,
+                                 const ephdc_seed *seed, ephdc_model **out) {
     if (!c || !sk || !class_hv || !out) return EPHDC_ENULL;
     *out = nullptr;
+    ephdc_seed key;
+    if (ephdc_status e = resolve_seed(seed, &key)) return e;
     if (sk->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
     const uint32_t N = c->N, L = c->L, D = c->p.D_live, k = c->p.k;
     for (size_t i = 0; i < (size_t)k * D; ++i)
@@ -415,7 +466,7 @@ ephdc_status ephdc_encrypt_model(const ephdc_ctx *c, const ephdc_sk *sk, const i
     for (uint32_t d0 = 0; d0 < D; d0 += chunk) {
         const uint32_t nd = std::min(chunk, D - d0);
         EPHDC_CUDA_TRY(launch_pack_intt_model(c, (const int8_t *)bC.p, d0, nd, (uint32_t *)bM.p, st));
-        EPHDC_CUDA_TRY(launch_encrypt(c, (const uint32_t *)bM.p, d0, nd, (const uint64_t *)bS.p, seed,
+        EPHDC_CUDA_TRY(launch_encrypt(c, (const uint32_t *)bM.p, d0, nd, (const uint64_t *)bS.p, key,
                                       m->d_ct + (size_t)d0 * L * 2 * N, st));
     }
     // FP64 path: keep the residues as exact doubles (the fused kernel's operand format)
@@ -699,8 +750,11 @@ ephdc_status ephdc_classify_host(const ephdc_ctx *c, const ephdc_model *m, ephdc
 // HE-HDC-SR, the server-side SIMD baseline
 // ------------------------------------------------------------------------------------
 ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *c, ephdc_sk *sk, ephdc_workspace *ws, const int8_t *d_H,
-                                      uint32_t nq, uint32_t b, uint64_t seed, uint64_t *d_qct, void *stream) {
+                                      uint32_t nq, uint32_t b, const ephdc_seed *seed, uint64_t *d_qct,
+                                      void *stream) {
     if (!c || !sk || !ws || !d_H || !d_qct) return EPHDC_ENULL;
+    ephdc_seed key;
+    if (ephdc_status e = resolve_seed(seed, &key)) return e;
     if (sk->ctx != c || ws->ctx != c || c->device < 0) return EPHDC_ECONTEXT;
     if ((uint64_t)b * c->B >= nq) return EPHDC_EPARAM;
     EPHDC_CUDA_TRY(cudaSetDevice(c->device));
@@ -713,7 +767,7 @@ ephdc_status ephdc_sr_encrypt_queries(const ephdc_ctx *c, ephdc_sk *sk, ephdc_wo
     const uint32_t D = c->p.D_live;
     EPHDC_CUDA_TRY(launch_pack_intt_sr(c, d_H, false, nq, b, 0, D, ws->d_M, st));
     // stream indices 2^32 + b*D + d: disjoint from the model's d < D_live (reading #25)
-    EPHDC_CUDA_TRY(launch_encrypt(c, ws->d_M, (1ull << 32) + (uint64_t)b * D, D, sk->d_shat_mont, seed, d_qct, st));
+    EPHDC_CUDA_TRY(launch_encrypt(c, ws->d_M, (1ull << 32) + (uint64_t)b * D, D, sk->d_shat_mont, key, d_qct, st));
     return EPHDC_OK;
 }
 

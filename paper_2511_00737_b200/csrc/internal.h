@@ -164,10 +164,10 @@ cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64
 cudaError_t launch_finalize(const ephdc_ctx *c, uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32_t nd, uint64_t *d_pt,
                                  cudaStream_t st);
-// secret-key encryption of nd encoded messages d_M ([0, t)): random streams g0 + dd,
-// output d_out [nd][L][2][N]
+// secret-key encryption of nd encoded messages d_M ([0, t)): random streams g0 + dd
+// under the ChaCha20 key (rng.cuh), output d_out [nd][L][2][N]
 cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint64_t g0, uint32_t nd,
-                           const uint64_t *d_shat_mont, uint64_t seed, uint64_t *d_out, cudaStream_t st);
+                           const uint64_t *d_shat_mont, const ephdc_seed &key, uint64_t *d_out, cudaStream_t st);
 cudaError_t launch_pack_intt_sr(const ephdc_ctx *c, const int8_t *src, bool model, uint32_t nq, uint32_t b,
                                 uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st);
 cudaError_t launch_mac_ctx(const ephdc_ctx *c, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D, uint64_t *d_out,

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>())
 struct EncArgs {
     PrimeSet ps;
     u32 L;
-    u64 seed;
+    ephdc_rng::Key key;
     const u64 *cdt;
     const u64 *shat_mont;   // [L][N], s_hat * 2^64 mod q
     const TwPair<u64> *tw;  // [L][N]
@@ -383,10 +383,10 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>())
     const u64 d = g0 + dd;   // random-stream index (model: d; HE-HDC-SR queries: 2^32 + b D + d)
     const u64 q = a.ps.q[j], delta = a.ps.delta[j], delta_p = a.ps.delta_p[j];
     const u32 *m = M + (size_t)dd * N;
-    const u64 seed = a.seed;
+    const ephdc_rng::Key &key = a.key;
     auto load = [&](int pos) -> u64 {
         const u64 x = mul_shoup_lazy<u64>((u64)m[pos], delta, delta_p, q);  // Delta*m in [0, 2q)
-        const int e = ephdc_rng::gaussian(seed, d, (u32)pos, cdt);
+        const int e = ephdc_rng::gaussian(key, d, (u32)pos, cdt);
         return e >= 0 ? x + (u64)e : x + q - (u64)(-e);                     // [0, 4q)
     };
     fwd_ntt<u64, LG, E>(buf, load, a.tw + (size_t)j * N, (u32)N, q);
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>())
     for (int e = 0; e < E; ++e) {
         const int pos = threadIdx.x + e * NT;
         const u64 xh = reduce4<u64>(buf[pad(pos)], q, 2 * q);
-        const u64 av = ephdc_rng::uniform_mod(seed, d, j, a.L, (u32)pos, q, mask);
+        const u64 av = ephdc_rng::uniform_mod(key, d, j, a.L, (u32)pos, q, mask);
         const u64 as = mont_mul(av, sh[pos], q, a.ps.qinv[j]);
         c0[pos] = xh >= as ? xh - as : xh + q - as;
         c1[pos] = av;
@@ -798,8 +798,8 @@ cudaError_t launch_plaintext_ntt(const ephdc_ctx *c, const uint32_t *d_M, uint32
 }
 
 template <int LG>
-static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u64 d0, u32 nd, const u64 *shat, u64 seed, u64 *model,
-                              cudaStream_t st) {
+static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u64 d0, u32 nd, const u64 *shat, const ephdc_seed &key,
+                              u64 *model, cudaStream_t st) {
     const size_t smem = sizeof(u64) * padded_len(1 << LG);
     auto kern = k_encrypt<LG>;
     cudaError_t e = set_smem(kern, smem);
@@ -807,7 +807,7 @@ static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u64 d0, u32 nd, 
     EncArgs a;
     a.ps = c->ps;
     a.L = c->L;
-    a.seed = seed;
+    for (int i = 0; i < 8; ++i) a.key.k[i] = key.key[i];
     a.cdt = c->dev.cdt;
     a.shat_mont = shat;
     a.tw = c->dev.tw_q;
@@ -816,14 +816,14 @@ static cudaError_t enc_launch(const ephdc_ctx *c, const u32 *M, u64 d0, u32 nd, 
 }
 
 cudaError_t launch_encrypt(const ephdc_ctx *c, const uint32_t *d_M, uint64_t d0, uint32_t nd,
-                           const uint64_t *d_shat_mont, uint64_t seed, uint64_t *d_model, cudaStream_t st) {
+                           const uint64_t *d_shat_mont, const ephdc_seed &key, uint64_t *d_model, cudaStream_t st) {
     if (nd == 0) return cudaSuccess;
     switch (c->p.log2N) {
-        case 10: return enc_launch<10>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
-        case 11: return enc_launch<11>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
-        case 12: return enc_launch<12>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
-        case 13: return enc_launch<13>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
-        case 14: return enc_launch<14>(c, d_M, d0, nd, d_shat_mont, seed, d_model, st);
+        case 10: return enc_launch<10>(c, d_M, d0, nd, d_shat_mont, key, d_model, st);
+        case 11: return enc_launch<11>(c, d_M, d0, nd, d_shat_mont, key, d_model, st);
+        case 12: return enc_launch<12>(c, d_M, d0, nd, d_shat_mont, key, d_model, st);
+        case 13: return enc_launch<13>(c, d_M, d0, nd, d_shat_mont, key, d_model, st);
+        case 14: return enc_launch<14>(c, d_M, d0, nd, d_shat_mont, key, d_model, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -15,7 +15,7 @@ import numpy as np
 import ephdc_inputs as inp
 from . import Context, EncryptedModel, SecretKey, encode_raw, find_ntt_primes, query_bits, train_model
 
-SK_SEED_OFFSET = 17      # same seed schedule as the oracle's driver (inputs, not arithmetic)
+SK_SEED_OFFSET = 17      # deterministic test keys: the oracle driver's seed schedule (inputs, not arithmetic)
 ENC_SEED_OFFSET = 29
 
 
@@ -49,9 +49,13 @@ def make_context(cfg: inp.Config, t: int, q, Qbits: int, qshift: int, device: in
 
 def build(cfg: inp.Config, P: np.ndarray, X_train: np.ndarray, y_train: np.ndarray, device: int = 0,
           sk_seed: Optional[int] = None, enc_seed: Optional[int] = None, arith: int = 0,
-          encoder: int = 0) -> Setup:
+          encoder: int = 0, deterministic: bool = False) -> Setup:
     """arith: 0 auto (FP64 pipe when eligible), 1 integer pipe, 2 FP64 pipe (ephdc_params.arith);
-    encoder: 0 auto (tcgen05 tensor cores), 1 dp4a CUDA cores (ephdc_params.encoder)."""
+    encoder: 0 auto (tcgen05 tensor cores), 1 dp4a CUDA cores (ephdc_params.encoder).
+    Keys (reading #7): by default the secret key and the model encryption each draw a
+    fresh OS key; deterministic=True (parity tests, benchmarks) uses the guessable test
+    keys cfg.seed + 17 / + 29 -- the oracle driver's schedule -- unless sk_seed / enc_seed
+    name others."""
     import torch
     dev = torch.device("cuda", device)
     t, q = primes_for(cfg)
@@ -65,6 +69,9 @@ def build(cfg: inp.Config, P: np.ndarray, X_train: np.ndarray, y_train: np.ndarr
     class_hv, qshift = train_model(acc, y_train, cfg.k, cfg.Cbits, Qbits)
     ctx0.close()
     ctx = make_context(cfg, t, q, Qbits, qshift, device, arith, encoder)
-    sk = SecretKey(ctx, cfg.seed + SK_SEED_OFFSET if sk_seed is None else sk_seed)
-    model = EncryptedModel(ctx, sk, class_hv, cfg.seed + ENC_SEED_OFFSET if enc_seed is None else enc_seed)
+    if deterministic:
+        sk_seed = cfg.seed + SK_SEED_OFFSET if sk_seed is None else sk_seed
+        enc_seed = cfg.seed + ENC_SEED_OFFSET if enc_seed is None else enc_seed
+    sk = SecretKey(ctx, sk_seed)
+    model = EncryptedModel(ctx, sk, class_hv, enc_seed)
     return Setup(cfg, ctx, sk, model, class_hv, P_dev, Qbits, qshift)

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(_capi.lib, s), s
     assert set(syms) == set(_capi.EXPORTED)
-    assert _capi.lib.ephdc_abi_version() == 2
+    assert _capi.lib.ephdc_abi_version() == 3
 
 
 def test_library_is_sm100a_only():
@@ -109,6 +109,29 @@ def test_keygen_matches_oracle(name):
     s, sh = sk.export()
     assert np.array_equal(s, bfv.keygen(1234))
     assert np.array_equal(sh, bfv.s_hat)
+
+
+def test_chacha20_block_known_answers():
+    """The library's generator (rng.cuh, host side) against RFC 8439's known answers."""
+    import json, os, struct
+    gold = os.path.join(os.path.dirname(__file__), "golden", "chacha20_kat.json")
+    for v in json.load(open(gold))["vectors"]:
+        nonce = struct.unpack("<3I", bytes.fromhex(v["nonce"]))
+        want = np.array(struct.unpack("<16I", bytes.fromhex(v["block"])), dtype=np.uint32)
+        assert np.array_equal(eph.chacha20_block(bytes.fromhex(v["key"]), v["counter"], nonce), want), v["source"]
+
+
+def test_keys_default_to_os_entropy():
+    """No seed: every key is fresh (ephdc_seed_os); an int seed is the deterministic test key."""
+    _, bfv, ctx = _host_ctx("c1q3")
+    s1, s2 = eph.SecretKey(ctx).export()[0], eph.SecretKey(ctx).export()[0]
+    assert not np.array_equal(s1, s2)
+    for s in (s1, s2):
+        assert set(np.unique(s)) <= {-1, 0, 1} and abs((s == 0).mean() - 1 / 3) < 0.1
+    key = (1234).to_bytes(8, "little") + bytes(24)     # ephdc_seed_u64(v) = (lo32, hi32, 0, ..., 0)
+    assert np.array_equal(eph.SecretKey(ctx, key).export()[0], bfv.keygen(1234))
+    with pytest.raises(ValueError):
+        eph.make_seed(b"short")
 
 
 @pytest.mark.parametrize("name,nq", [("c1q3", 700), ("c2", 300)])

@@ -47,7 +47,7 @@ def test_fullsize_step_parity(name):
     nq = cfg.nq
     Xtr, ytr, Xq, _ = inp.gen_features(cfg)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, deterministic=True)
     assert ps.ctx.arith == "f64"
     H, got = _run_step(ps, cfg, Xq, nq)
     nb = got.shape[0]
@@ -70,7 +70,7 @@ def test_fullsize_step_parity(name):
     # the integer-pipe fused kernel on the same full-size step
     del ps
     torch.cuda.empty_cache()
-    ps_int = ppipe.build(cfg, P, Xtr, ytr, arith=1)
+    ps_int = ppipe.build(cfg, P, Xtr, ytr, arith=1, deterministic=True)
     assert ps_int.ctx.arith == "int"
     _, got_int = _run_step(ps_int, cfg, Xq, nq)
     assert np.array_equal(got_int, got)
@@ -85,7 +85,7 @@ def test_int_path_large_primes_n16384():
     nq = cfg.nq
     Xtr, ytr, Xq, _ = inp.gen_features(cfg)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, deterministic=True)
     assert ps.ctx.arith == "int"
     assert max(ps.ctx.q) >= 1 << 50
     H, got = _run_step(ps, cfg, Xq, nq)

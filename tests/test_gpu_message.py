@@ -21,7 +21,7 @@ from paper_2511_00737_b200 import pipeline as ppipe  # noqa: E402
 def test_message_bitexact(name, nq):
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, _ = inp.gen_features(cfg, nq)
-    ps = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr)
+    ps = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr, deterministic=True)
     ctx = ps.ctx
     ws = eph.Workspace(ctx, nq)
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()

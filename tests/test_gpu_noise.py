@@ -31,7 +31,7 @@ def _setup(name, nq):
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, _ = inp.gen_features(cfg, nq)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, deterministic=True)
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)
     ws = eph.Workspace(ps.ctx, nq)
@@ -81,11 +81,11 @@ def test_probe_at_failing_literal_c1():
 def test_probe_empty_and_errors():
     cfg = inp.CONFIGS["c1q3"]
     Xtr, ytr, _, _ = inp.gen_features(cfg, 4)
-    ps = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr)
+    ps = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr, deterministic=True)
     empty = torch.empty((0, 2, ps.ctx.L, ps.ctx.N), dtype=torch.int64, device="cuda")
     bits, flags, lg = eph.noise_probe(ps.ctx, ps.sk, empty)
     assert bits.size == 0
-    other = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr)
+    other = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr, deterministic=True)
     ct = torch.zeros((1, 2, ps.ctx.L, ps.ctx.N), dtype=torch.int64, device="cuda")
     with pytest.raises(eph.EphdcError) as e:
         eph.noise_probe(ps.ctx, other.sk, ct)

@@ -37,7 +37,7 @@ def setup(name, nq, arith="auto"):
     Xtr, ytr, Xq, yq = inp.gen_features(cfg, nq)
     P = inp.gen_projection(cfg)
     om = opipe.build_model(cfg, P, Xtr, ytr)
-    ps = ppipe.build(cfg, P, Xtr, ytr, arith=ARITH[arith])
+    ps = ppipe.build(cfg, P, Xtr, ytr, arith=ARITH[arith], deterministic=True)
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H_dev = eph.encode_queries(ps.ctx, X, ps.P_dev)
     torch.cuda.synchronize()
@@ -172,7 +172,7 @@ def test_slot_packing_small_k(k, nq):
     Xtr, ytr, Xq, _ = inp.gen_features(cfg, nq)
     P = inp.gen_projection(cfg)
     om = opipe.build_model(cfg, P, Xtr, ytr)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, deterministic=True)
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)
     ws = eph.Workspace(ps.ctx, nq)

@@ -29,7 +29,7 @@ def test_scaled_model_matches_sequential_oracle(name, nq, g, scales, arith):
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, _ = inp.gen_features(cfg, nq)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr, arith=arith)
+    ps = ppipe.build(cfg, P, Xtr, ytr, arith=arith, deterministic=True)
     ps.model.scale(g, scales)
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)
@@ -45,7 +45,7 @@ def test_scaled_model_matches_sequential_oracle(name, nq, g, scales, arith):
 def test_model_scale_rejects_bad_schedules():
     cfg = inp.CONFIGS["c1q3"]
     Xtr, ytr, _, _ = inp.gen_features(cfg, 4)
-    ps = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr)
+    ps = ppipe.build(cfg, inp.gen_projection(cfg), Xtr, ytr, deterministic=True)
     for g, scales in ((512, [1]), (0, []), (512, [1, 65537])):
         with pytest.raises(eph.EphdcError) as e:
             ps.model.scale(g, scales)

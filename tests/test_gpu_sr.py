@@ -22,7 +22,7 @@ def test_sr_bitexact(name, nq, arith):
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, _ = inp.gen_features(cfg, nq)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr, arith=arith)
+    ps = ppipe.build(cfg, P, Xtr, ytr, arith=arith, deterministic=True)
     ctx = ps.ctx
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H = eph.encode_queries(ctx, X, ps.P_dev)

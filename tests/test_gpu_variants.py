@@ -49,7 +49,7 @@ def test_plan_variants_bit_identical(name, extra):
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, _ = inp.gen_features(cfg)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, deterministic=True)
     assert ps.ctx.arith == "f64"
     nq = 2 * ps.ctx.B + extra                      # 3 batches, the last ragged
     Xs = np.ascontiguousarray(Xq[:nq])
@@ -74,7 +74,7 @@ def test_batch_groups_bit_identical(name, groups):
     cfg = inp.CONFIGS[name]
     Xtr, ytr, Xq, _ = inp.gen_features(cfg)
     P = inp.gen_projection(cfg)
-    ps = ppipe.build(cfg, P, Xtr, ytr)
+    ps = ppipe.build(cfg, P, Xtr, ytr, deterministic=True)
     nq = 5 * ps.ctx.B + 11 if name == "c3" else 15 * ps.ctx.B + 7
     X = torch.from_numpy(np.ascontiguousarray(Xq[:nq]).view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)

@@ -93,11 +93,50 @@ def test_brev():
             assert nt.brev(nt.brev(i, bits), bits) == i
 
 
-def test_splitmix64_known_answer():
-    kat = json.load(open(os.path.join(GOLD, "splitmix64_kat.json")))
+def _kat_vectors():
+    import struct
+    for v in json.load(open(os.path.join(GOLD, "chacha20_kat.json")))["vectors"]:
+        key = np.array(struct.unpack("<8I", bytes.fromhex(v["key"])), dtype=np.uint32)
+        nonce = np.array(struct.unpack("<3I", bytes.fromhex(v["nonce"])), dtype=np.uint32)
+        want = np.array(struct.unpack("<16I", bytes.fromhex(v["block"])), dtype=np.uint32)
+        yield v, key, nonce, want
+
+
+def test_chacha20_known_answers():
+    """RFC 8439 sec. 2.3.2 and A.1 #1 pin the oracle's block function (reading #7)."""
     L = core.lib()
-    got = [L.or_draw(kat["seed"], n) for n in range(5)]
-    assert got == [int(v) for v in kat["outputs"]]
+    for v, key, nonce, want in _kat_vectors():
+        out = np.zeros(16, dtype=np.uint32)
+        L.or_chacha20_block(core.ptr(key), v["counter"], core.ptr(nonce), core.ptr(out))
+        assert np.array_equal(out, want), v["source"]
+
+
+def test_word64_is_block_word():
+    """or_word64 = little-endian word w of the block under key (lo, hi, 0..0), nonce (tag, a)."""
+    L = core.lib()
+    seed, tag, a = 0x0123456789ABCDEF, 3, (7 << 32) | 11
+    key = np.array([seed & 0xFFFFFFFF, seed >> 32, 0, 0, 0, 0, 0, 0], dtype=np.uint32)
+    nonce = np.array([tag, a & 0xFFFFFFFF, a >> 32], dtype=np.uint32)
+    for ctr in (0, 5):
+        b = np.zeros(16, dtype=np.uint32)
+        L.or_chacha20_block(core.ptr(key), ctr, core.ptr(nonce), core.ptr(b))
+        for w in range(8):
+            assert L.or_word64(seed, tag, a, ctr, w) == int(b[2 * w]) | (int(b[2 * w + 1]) << 32)
+
+
+def test_uniform_rejection_path():
+    """q just above a power of two: about half the first draws are rejected, the retry
+    stream fills them, and the result is still uniform on [0, q)."""
+    L = core.lib()
+    q = (1 << 20) + 7                     # mask = 2^21 - 1
+    N = 1 << 14
+    a = np.array([L.or_uniform_mod(9, 4, 1, 3, i, q) for i in range(N)], dtype=np.int64)
+    assert a.max() < q and a.min() >= 0
+    first = np.array([L.or_word64(9, 3, 4 * 3 + 1, i // 8, i % 8) & ((1 << 21) - 1) for i in range(N)])
+    acc = first < q
+    assert 0.4 < acc.mean() < 0.6
+    assert np.array_equal(a[acc], first[acc])          # accepted first draws are kept as drawn
+    assert abs(a.mean() / q - 0.5) < 0.02 and abs(a[~acc].mean() / q - 0.5) < 0.03
 
 
 def test_gaussian_cdt_pins():
@@ -141,3 +180,17 @@ def test_sampler_statistics():
     L.or_sample_uniform_poly(5, 2, 1, 9, q, N, core.ptr(a))
     assert int(a.max()) < q
     assert abs(a.astype(np.float64).mean() / q - 0.5) < 0.02
+
+
+def test_poly_samplers_match_coefficient_samplers():
+    """or_sample_*_poly (one block per 8 / 4 coefficients) = the per-coefficient definitions."""
+    L = core.lib()
+    N = 1 << 10
+    for q in ((1 << 20) + 7, 281474976546817):
+        a = np.empty(N, dtype=np.uint64)
+        L.or_sample_uniform_poly(11, 6, 2, 5, q, N, core.ptr(a))
+        assert [int(v) for v in a] == [L.or_uniform_mod(11, 6, 2, 5, i, q) for i in range(N)]
+    T = np.ascontiguousarray(gaussian_cdt(3.2))
+    e = np.empty(N, dtype=np.int64)
+    L.or_sample_gauss_poly(11, (1 << 32) + 3, N, core.ptr(T), 20, core.ptr(e))
+    assert [int(v) for v in e] == [L.or_gauss(11, (1 << 32) + 3, i, core.ptr(T), 20) for i in range(N)]

@@ -72,7 +72,7 @@ def main():
 
         def sr_client():
             eph.encode_queries(ctx, X, ps.P_dev, H)
-            eph.sr_encrypt_queries(ctx, ps.sk, ws, H, nq, 0, 4242, qct)
+            eph.sr_encrypt_queries(ctx, ps.sk, ws, H, nq, 0, None, qct)
 
         def sr_server():
             eph.sr_evaluate(ctx, pt, qct, res)

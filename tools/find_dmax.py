@@ -140,7 +140,10 @@ def main():
         for logN, qb in GRID:
             Ts = []
             for T in range(29, 10, -1):   # predicted D_max from ~1/4 to 2 D_cap
-                t = eph.find_ntt_primes(logN, [T])[0]
+                try:
+                    t = eph.find_ntt_primes(logN, [T])[0]
+                except eph.EphdcError:      # no prime = 1 mod 2N below 2^T
+                    break
                 if t.bit_length() != T:
                     continue
                 q = eph.find_ntt_primes(logN, list(qb), exclude=[t])
