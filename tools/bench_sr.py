@@ -8,7 +8,8 @@ HE-HDC-SR client = encode_queries + sr_encrypt_queries (D ciphertexts) for B que
 HE-HDC-SR server = sr_evaluate (D MulCP with plaintext class tiles)
 Messages: EP-HDC sends one scores ciphertext (bit-packed, ephdc_scores_message_bytes);
 HE-HDC-SR uploads D ciphertexts (same packing) and receives one.
-CUDA-event times, warm-up 3, median of 5.
+CUDA-event times, warm-up 3, median of >= 5 repetitions spanning >= 0.6 s, each
+measurement with the nvidia-smi clock record of its timed region (bench.ClockSampler).
 
 usage: python tools/bench_sr.py [--configs c2 c3 c4]
 """
@@ -27,19 +28,23 @@ sys.path.insert(0, ROOT)
 
 
 def timed(fn, reps=5, warm=3):
+    """(median ms, clock record): >= reps repetitions and >= 0.6 s under the sampler."""
     import torch
+    from bench import ClockSampler
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    clk = ClockSampler(0)
+    clk.start()
     ts = []
-    for _ in range(reps):
+    while len(ts) < reps or sum(ts) < 600.0:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    return statistics.median(ts)
+    return statistics.median(ts), clk.stop()
 
 
 def main():
@@ -77,13 +82,14 @@ def main():
         def sr_server():
             eph.sr_evaluate(ctx, pt, qct, res)
 
-        t_ep, t_src, t_srs = timed(ep_client), timed(sr_client), timed(sr_server)
+        (t_ep, c_ep), (t_src, c_src), (t_srs, c_srs) = timed(ep_client), timed(sr_client), timed(sr_server)
         msg1 = eph.scores_message_bytes(ctx, 1)
         line = {"workload": name, "queries_per_batch": nq, "N": ctx.N, "L": ctx.L, "D": cfg.D_live,
                 "ep_hdc_client_ms": round(t_ep, 3), "he_hdc_sr_client_ms": round(t_src, 3),
                 "he_hdc_sr_server_ms": round(t_srs, 3), "client_ratio_sr_over_ep": round(t_src / t_ep, 2),
                 "ep_hdc_upload_bytes": msg1, "he_hdc_sr_upload_bytes": msg1 * cfg.D_live,
                 "message_ratio": cfg.D_live,
+                "clocks": {"ep_hdc_client": c_ep, "he_hdc_sr_client": c_src, "he_hdc_sr_server": c_srs},
                 "paper": "P:778-786 (Ryzen 3970X, 1 core, Pyfhel): SR client 351.95 ms vs EP 43.99 ms at N=2^11 D=1K"}
         print(json.dumps(line), flush=True)
         del qct, pt, out, H, X, ws, ps
