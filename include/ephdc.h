@@ -383,10 +383,14 @@ ephdc_status ephdc_noise_probe(const ephdc_ctx *ctx, const ephdc_sk *sk, const u
 /* Tables for L primes (each = 1 mod 2N, < 2^61) at ring degree N = 2^log2N,
  * 10 <= log2N <= 16, on `device`.  flags: 0 = the tuned kernels (FP64 pipe where
  * the bounds of DESIGN.md 5.1 hold, else the integer pipe); EPHDC_NTT_FORCE_INT =
- * the integer-pipe kernels everywhere (TEST/PROFILING: bit-identical results).
+ * the integer-pipe kernels everywhere; EPHDC_NTT_ALT_TEAMS = at N = 2^13 the other
+ * warp layout of the c5 kernels (forward: one 16-warp team instead of two 8-warp
+ * groups; inverse: two groups instead of one team) (TEST/PROFILING only, both:
+ * bit-identical results).
  * Synchronous.  Errors: ENULL, EPARAM (sizes, a q_j that is not an NTT prime, unknown
  * flags), ECONTEXT (device < 0), ECUDA, ERESOURCE. */
 #define EPHDC_NTT_FORCE_INT 1u
+#define EPHDC_NTT_ALT_TEAMS 2u
 ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device,
                                    uint32_t flags, ephdc_ntt_plan **out);
 void ephdc_ntt_plan_free(ephdc_ntt_plan *p);

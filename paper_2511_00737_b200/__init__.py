@@ -423,16 +423,18 @@ def noise_probe(ctx: Context, sk: SecretKey, cts, stream=None) -> Tuple[np.ndarr
 
 # --------------------------------------------------------------------------- standalone (c5)
 class NttPlan:
-    """ephdc_ntt_plan.  force_int: the integer-pipe kernels everywhere (tests/profiling,
-    EPHDC_NTT_FORCE_INT; bit-identical results)."""
+    """ephdc_ntt_plan.  force_int: the integer-pipe kernels everywhere (EPHDC_NTT_FORCE_INT);
+    alt_teams: the other warp layout of the c5 kernels at N = 2^13 (EPHDC_NTT_ALT_TEAMS).  Both are
+    tests/profiling switches with bit-identical results."""
 
-    def __init__(self, q: Sequence[int], log2N: int, device: int = 0, force_int: bool = False):
+    def __init__(self, q: Sequence[int], log2N: int, device: int = 0, force_int: bool = False,
+                 alt_teams: bool = False):
         self.q = [int(x) for x in q]
         self.L, self.log2N, self.N = len(q), log2N, 1 << log2N
         qa = np.ascontiguousarray(np.array(self.q, dtype=np.uint64))
         self._h = ctypes.c_void_p()
-        call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device, 1 if force_int else 0,
-             ctypes.byref(self._h))
+        call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device,
+             (1 if force_int else 0) | (2 if alt_teams else 0), ctypes.byref(self._h))
         info = (ctypes.c_uint32 * 3)()
         call("ephdc_ntt_plan_query", self._h, ctypes.addressof(info))
         names = {0: "int", 1: "f64", 2: "c5_f64"}

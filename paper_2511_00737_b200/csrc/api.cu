@@ -960,7 +960,8 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
                                    ephdc_ntt_plan **out) {
     if (!q || !out) return EPHDC_ENULL;
     *out = nullptr;
-    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16 || (flags & ~EPHDC_NTT_FORCE_INT)) return EPHDC_EPARAM;
+    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16 || (flags & ~(EPHDC_NTT_FORCE_INT | EPHDC_NTT_ALT_TEAMS)))
+        return EPHDC_EPARAM;
     for (uint32_t j = 0; j < L; ++j)
         if (q[j] >= (1ull << 61) || !is_ntt_prime(q[j], log2N)) return EPHDC_EPARAM;
     if (device < 0) return EPHDC_ECONTEXT;
@@ -989,6 +990,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
     }
     plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
     if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
+    p->c5_alt_teams = (flags & EPHDC_NTT_ALT_TEAMS) != 0;
     // the c5 kernels (ntt_c5.cu) use the FP64 forward table at every N >= 2^12 whose
     // primes are all < 2^50; their own bounds are decided in plan_ntt_c5
     const bool c5_candidate = !(flags & EPHDC_NTT_FORCE_INT) && log2N >= 12 &&

@@ -79,7 +79,10 @@ template <int LGC, int S> constexpr size_t mac_f64_smem() {
 template <int LGC, int E> constexpr int mac_threads() { return (1 << LGC) / E; }
 template <int LGC, int E> constexpr int mac_min_blocks() { return E == kE ? f64_ctas_per_sm<LGC>() : 1; }
 
-template <int LGC, int S, int WL, int E>
+// PREFIX (ephdc_infer_batch_prefix): batch b sums only its first dlim[b] dims.  A
+// separate instantiation: even this one clamp reschedules the whole 128-register kernel
+// (ptxas) and cost the default path 6% at c4 (r02: 260.4 vs 245 ms).
+template <int LGC, int S, int WL, int E, bool PREFIX = false>
 __global__ void __launch_bounds__(mac_threads<LGC, E>(), mac_min_blocks<LGC, E>())
     k_ntt_mac_f64(const u32 *__restrict__ M, const double *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
     using namespace ephdc_async;
@@ -114,8 +117,7 @@ __global__ void __launch_bounds__(mac_threads<LGC, E>(), mac_min_blocks<LGC, E>(
     const u32 chunk = x % a.chunks, grp = x / a.chunks;
     const u32 b = grp * a.bg + bl;
     if (b >= a.nb) return;
-    // dlim (ephdc_infer_batch_prefix): batch b sums only its first dlim[b] dims
-    const u32 d0 = chunk * a.G, d1 = min(a.dlim ? min(a.D, a.dlim[b]) : a.D, d0 + a.G);
+    const u32 d0 = chunk * a.G, d1 = PREFIX ? min(min(a.D, a.dlim[b]), d0 + a.G) : min(a.D, d0 + a.G);
     if (d0 >= d1) return;
 
     const u32 *Mb = M + (size_t)b * a.D * N;
@@ -675,8 +677,9 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     if (env & 1u) prefetch = false;
     if (env & 16u) prefetch = true;
     const bool e32 = LGC == 13 && (env & 8u) != 0;
-    auto kern = e32 ? (wl == 2 ? k_ntt_mac_f64<LGC, S, 2, 32> : k_ntt_mac_f64<LGC, S, 1, 32>)
-                    : wl == 0 ? k_ntt_mac_f64<LGC, S, 0, kE> : wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;
+    auto kern = dlim ? (wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE, true> : k_ntt_mac_f64<LGC, S, 1, kE, true>)
+                : e32 ? (wl == 2 ? k_ntt_mac_f64<LGC, S, 2, 32> : k_ntt_mac_f64<LGC, S, 1, 32>)
+                      : wl == 0 ? k_ntt_mac_f64<LGC, S, 0, kE> : wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;
     cudaError_t e = smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
     F64MacArgs a = f64_args(c);
@@ -694,7 +697,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     const uint64_t groups = (nb + a.bg - 1) / a.bg;
     const uint64_t grid = groups * a.chunks * a.bg * c->L * S;
     if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-    kern<<<(unsigned)grid, (1 << LGC) / (e32 ? 32 : kE), smem, st>>>(M, model, out, a);
+    kern<<<(unsigned)grid, (1 << LGC) / (e32 && !dlim ? 32 : kE), smem, st>>>(M, model, out, a);
     return counted(cudaGetLastError());
 }
 

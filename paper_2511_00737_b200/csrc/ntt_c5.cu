@@ -62,13 +62,7 @@ __host__ __device__ constexpr int sw(int e) { return e ^ (((e >> 4) & 7) << 1); 
 template <int LGC> constexpr int ctas_per_sm() { return LGC <= 12 ? 2 : 1; }
 template <int LGC> constexpr uint32_t tmem_cols() { return 128u * (uint32_t)(((1 << LGC) / kE / 32 + 3) / 4); }
 
-EPHDC_D double centered(u64 v, double q) {   // [0, q) -> (-q/2, q/2]
-    const double x = from_u64(v);
-    return x > 0.5 * q ? __dsub_rn(x, q) : x;
-}
-EPHDC_D u64 out_u64(double x, double q, double nq, double qinv) {   // |x| < 2^53 -> [0, q)
-    return to_canonical_u64(reduce(x, qinv, nq), q);
-}
+
 
 EPHDC_D void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
     asm volatile(
@@ -143,7 +137,30 @@ struct Ctx {
     uint32_t tbase;    // this thread's TMEM columns
     int tid, warp, lane;
     double q, nq, qinv;
+    u64 qi;            // q as an integer
+    EPHDC_D void set_prime(double2 qq) {   // (q, fl(1/q)) = entry 0 of a twiddle table
+        q = qq.x;
+        nq = -qq.x;
+        qinv = qq.y;
+        qi = (u64)q;
+    }
 };
+
+// Input centering and output canonicalisation as 64-bit integer selects on the idle
+// integer pipe; one FP64 operation converts each way (2 + 2 fewer FP64 operations per
+// element than FP64 compare/select forms; r14 A/B: +1.5% at 2^14, equal at 2^13).
+// kRound = 1.5 * 2^52 has the bit pattern 0x4338000000000000 and a unit last place, so
+// for an integer |c| < 2^51 the pattern 0x4338000000000000 + c IS the double kRound + c.
+constexpr long long kRoundBits = 0x4338000000000000LL;
+EPHDC_D double centered(u64 v, const Ctx &f) {   // [0, q) -> (-q/2, q/2]
+    const long long c = (long long)(v > (f.qi >> 1) ? v - f.qi : v);
+    return __dsub_rn(__longlong_as_double(kRoundBits + c), kRound);
+}
+EPHDC_D u64 out_u64(double x, const Ctx &f) {   // |x| < 2^51 -> [0, q)
+    const double k = __dadd_rn(__fma_rn(x, f.qinv, kRound), -kRound);
+    const long long r = __double_as_longlong(__fma_rn(k, f.nq, __dadd_rn(x, kRound))) - kRoundBits;   // x - k q
+    return (u64)r + (r < 0 ? f.qi : 0ull);
+}
 
 template <int LGC> EPHDC_D void frame_init(Ctx &f, unsigned char *smem_raw, int n_bufs, uint64_t *mbar,
                                            uint32_t *tmem_slot) {
@@ -255,25 +272,21 @@ template <int LGC> struct Fwd {
         for (int k = 0; k < 16; ++k) C[sb ^ sw(k * TL2)] = x[k];
     }
 
+    // (each group's TMEM twiddle load is issued before its shared-memory loads, so the
+    // two latencies overlap)
     static EPHDC_D void pass3(const Ctx &f, double *C) {
 #pragma unroll
         for (int u = 0; u < G3; ++u) {
             const int sb = sw(p3_blk(f, u) * NB8 + p3_off(f, u));
+            uint32_t rr[kP3Cols];
+            ephdc_tmem::ldx<16>(f.tbase + kP3Cols * u, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
+            if constexpr (R3 == 3)
+                ephdc_tmem::ldx<16>(f.tbase + kP3Cols * u + 16u, *reinterpret_cast<uint32_t(*)[16]>(&rr[16]));
             double x[1 << R3];
 #pragma unroll
             for (int k = 0; k < (1 << R3); ++k) x[k] = C[sb ^ sw(4 * k)];
-            if constexpr (R3 == 3) {
-                uint32_t rr[32];
-                ephdc_tmem::ldx<16>(f.tbase + kP3Cols * u, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
-                ephdc_tmem::ldx<16>(f.tbase + kP3Cols * u + 16u, *reinterpret_cast<uint32_t(*)[16]>(&rr[16]));
-                ephdc_tmem::waitx<32>(rr);
-                ct_stages<R3, 0, R3>(x, [&](int sub, int v) { return pair_at(rr, (1 << sub) - 1 + v); }, f.nq);
-            } else {
-                uint32_t rr[16];
-                ephdc_tmem::ldx<16>(f.tbase + kP3Cols * u, rr);
-                ephdc_tmem::waitx<16>(rr);
-                ct_stages<R3, 0, R3>(x, [&](int sub, int v) { return pair_at(rr, (1 << sub) - 1 + v); }, f.nq);
-            }
+            ephdc_tmem::waitx<kP3Cols>(rr);
+            ct_stages<R3, 0, R3>(x, [&](int sub, int v) { return pair_at(rr, (1 << sub) - 1 + v); }, f.nq);
 #pragma unroll
             for (int k = 0; k < (1 << R3); ++k) C[sb ^ sw(4 * k)] = x[k];
         }
@@ -296,8 +309,8 @@ template <int LGC> struct Fwd {
             ct_bfly(x1, x3, t0.x, t0.y, f.nq);
             ct_bfly(x0, x1, t1.x, t1.y, f.nq);
             ct_bfly(x2, x3, t2.x, t2.y, f.nq);
-            st_cs_v2(o + 4 * g4, out_u64(x0, f.q, f.nq, f.qinv), out_u64(x1, f.q, f.nq, f.qinv));
-            st_cs_v2(o + 4 * g4 + 2, out_u64(x2, f.q, f.nq, f.qinv), out_u64(x3, f.q, f.nq, f.qinv));
+            st_cs_v2(o + 4 * g4, out_u64(x0, f), out_u64(x1, f));
+            st_cs_v2(o + 4 * g4 + 2, out_u64(x2, f), out_u64(x3, f));
         }
     }
 };
@@ -336,9 +349,7 @@ __global__ void __launch_bounds__((1 << LGC) / kE, ctas_per_sm<LGC>())
             __syncthreads();
             const double2 *twg = a.tw + (size_t)j * NC;
             F::load_twiddles(f, [&](int m, int B) { return twg[m + B]; });
-            f.q = twg[0].x;
-            f.nq = -f.q;
-            f.qinv = twg[0].y;
+            f.set_prime(twg[0]);
             jcur = j;
             ephdc_tmem::fence_before_sync();
             __syncthreads();
@@ -351,7 +362,7 @@ __global__ void __launch_bounds__((1 << LGC) / kE, ctas_per_sm<LGC>())
             const int st = sw(f.tid);
             double x[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) x[k] = centered(Cu[st ^ sw(k * NT)], f.q);
+            for (int k = 0; k < 16; ++k) x[k] = centered(Cu[st ^ sw(k * NT)], f);
             F::pass1(f, C, x);
         }
         __syncthreads();
@@ -361,6 +372,106 @@ __global__ void __launch_bounds__((1 << LGC) / kE, ctas_per_sm<LGC>())
         F::pass3(f, C);
         __syncwarp();
         F::tail(f, C, poly_ptr(a, w));
+    }
+    frame_exit<LGC>(f, tmem_slot);
+}
+
+// ---------------------------------------------------------------------------------
+// Two warp groups per CTA (N = 2^13).  With one 16-warp team every warp reaches the
+// load and store phases of a pass at the same time (one barrier per item aligns them),
+// so the shared-memory traffic (4 passes x 16 B per element, ~4K of the ~12K clocks of
+// a polynomial) and the FP64 work serialise.  Here two 8-warp groups transform
+// alternate polynomials of the CTA's range, each thread doing the work of the 16-warp
+// version's threads tid and tid + 256 one after the other (same registers per thread,
+// same TMEM columns: warps w and w + 8 share a lane quarter and the twiddles), with a
+// group-local named barrier; group 1 starts one pass late, so one group's loads and
+// stores overlap the other's butterflies.  Items of one prime form a segment (both
+// groups hold that prime's twiddles); buffers rotate by three: item i's pass-1 barrier
+// frees buffer (i - 2) % 3 -- item i - 2 was the same group's (or a finished segment's)
+// -- for the TMA of item i + 1.
+// ---------------------------------------------------------------------------------
+EPHDC_D void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+EPHDC_D void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// the 16-warp thread tid + 256 h seen by thread tid of a group (warp w, lane quarter w % 4)
+EPHDC_D Ctx half_ctx(const Ctx &f, int h) {
+    Ctx v = f;
+    const int gw = (f.tid >> 5) & 7;
+    v.tid = (f.tid & 255) + 256 * h;
+    v.warp = gw + 8 * h;
+    v.tbase = f.tbase - (uint32_t)(f.warp >> 2) * 128u + (uint32_t)(v.warp >> 2) * 128u;
+    return v;
+}
+
+// [i0, i1) = the segment of local item i0: the items of its prime
+EPHDC_D u32 segment_end(const C5Args &a, u32 w0, u32 w1, u32 i0) {
+    const u32 j = (w0 + i0) / a.batch;
+    return min(w1, (j + 1) * a.batch) - w0;
+}
+
+__global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd2g(const __grid_constant__ CUtensorMap map,
+                                                        const __grid_constant__ C5Args a) {
+    constexpr int LGC = 13;
+    using F = Fwd<LGC>;
+    constexpr int NC = F::NC;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar[kNBuf];
+    __shared__ uint32_t tmem_slot;
+    Ctx f;
+    frame_init<LGC>(f, smem_raw, kNBuf, mbar, &tmem_slot);
+    const int g = f.warp >> 3, gt = f.tid & 255;
+    const u32 w0 = (u32)((u64)a.items * blockIdx.x / gridDim.x), w1 = (u32)((u64)a.items * (blockIdx.x + 1) / gridDim.x);
+    const u32 n = w1 - w0;
+    auto issue = [&](u32 i) {   // one thread
+        uint64_t *bar = &mbar[i % 3];
+        ephdc_async::fence_proxy_async();
+        ephdc_async::mbar_arrive_expect_tx(bar, (u32)(NC * 8));
+        double *c = f.bufs + (size_t)(i % 3) * NC;
+        const int row0 = poly_row(a, w0 + i);
+#pragma unroll
+        for (int r = 0; r < NC / 16; r += kBoxRows) tma_load_2d(c + 16 * r, &map, 0, row0 + r, bar);
+    };
+    if (f.tid == 0)
+        for (u32 i = 0; i < 3 && i < n; ++i) issue(i);
+    for (u32 i0 = 0; i0 < n;) {
+        const u32 i1 = segment_end(a, w0, w1, i0), j = (w0 + i0) / a.batch;
+        __syncthreads();   // both groups are done with the previous prime
+        const double2 *twg = a.tw + (size_t)j * NC;
+        F::load_twiddles(half_ctx(f, g), [&](int m, int B) { return twg[m + B]; });
+        f.set_prime(twg[0]);
+        ephdc_tmem::fence_before_sync();
+        __syncthreads();
+        ephdc_tmem::fence_after_sync();
+        const bool pair = i0 + 1 < i1;
+        if (g == 1 && pair) bar_sync(3, 512);   // start one pass behind group 0
+        for (u32 i = i0 + g; i < i1; i += 2) {
+            ephdc_async::mbar_wait(&mbar[i % 3], (i / 3) & 1u);
+            double *C = f.bufs + (size_t)(i % 3) * NC;
+            const u64 *Cu = reinterpret_cast<const u64 *>(C);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const Ctx v = half_ctx(f, h);
+                const int st = sw(v.tid);
+                double x[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) x[k] = centered(Cu[st ^ sw(k * F::NT)], v);
+                F::pass1(v, C, x);
+            }
+            bar_sync(1 + g, 256);
+            if (g == 0 && i == i0 && pair) bar_arrive(3, 512);
+            if (gt == 0 && i >= 2 && i + 1 < n) issue(i + 1);   // buffer (i-2) % 3 is free
+            u64 *o = poly_ptr(a, w0 + i);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const Ctx v = half_ctx(f, h);
+                F::pass2(v, C);
+                __syncwarp();
+                F::pass3(v, C);
+                __syncwarp();
+                F::tail(v, C, o);
+            }
+        }
+        i0 = i1;
     }
     frame_exit<LGC>(f, tmem_slot);
 }
@@ -404,9 +515,7 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl(const __grid_constant_
             const double2 *twg = a.tw + ((size_t)j << a.log2N);
             F::load_twiddles(f, [&](int m, int Bk) { return twg[C * m + (int)s * m + Bk]; });
             if (f.tid < C) xtw[f.tid] = twg[f.tid];
-            f.q = twg[0].x;
-            f.nq = -f.q;
-            f.qinv = twg[0].y;
+            f.set_prime(twg[0]);
             jcur = j;
             ephdc_tmem::fence_before_sync();
             __syncthreads();
@@ -424,7 +533,7 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl(const __grid_constant_
                 const int rl = f.tid + u * NT, r = (int)s * SL + rl;
                 double x[C];
 #pragma unroll
-                for (int k = 0; k < C; ++k) x[k] = centered(Su[sw(k * SL + rl)], f.q);
+                for (int k = 0; k < C; ++k) x[k] = centered(Su[sw(k * SL + rl)], f);
                 ct_stages<LC, 0, LC>(x, [&](int sub, int v) { return xtw[(1 << sub) + v]; }, f.nq);
                 const uint32_t off = (uint32_t)sw(r) * 8u;
 #pragma unroll
@@ -515,8 +624,8 @@ template <int LGC> struct Inv {
             const int sg = sw(4 * g4);
             const ulonglong2 ua = *reinterpret_cast<const ulonglong2 *>(C + sg);
             const ulonglong2 ub = *reinterpret_cast<const ulonglong2 *>(C + (sg ^ 2));
-            const double v0 = centered(ua.x, f.q), v1 = centered(ua.y, f.q), v2 = centered(ub.x, f.q),
-                         v3 = centered(ub.y, f.q);
+            const double v0 = centered(ua.x, f), v1 = centered(ua.y, f), v2 = centered(ub.x, f),
+                         v3 = centered(ub.y, f);
             double x0 = __dadd_rn(v0, v1), x1 = __dsub_rn(v0, v1), x2 = __dadd_rn(v2, v3), x3 = __dsub_rn(v2, v3);
             const double2 t2 = f.tws[2], t3 = f.tws[3];
             ct_bfly(x0, x2, t2.x, t2.y, f.nq);
@@ -552,31 +661,32 @@ template <int LGC> struct Inv {
 
     // D: the last four levels on elements tid + NT k; the last one fused with the scaling;
     // sink(k, value) receives element tid + NT k
+    // (TMEM loads issued ahead: the level twiddles before the shared-memory loads, each
+    // scaling block one block ahead of its use)
     template <class Sink> static EPHDC_D void pass_d(const Ctx &f, const double *C, double2 cloc, const Sink &sink) {
+        uint32_t rr[32], sc[2][16];
+        ephdc_tmem::ldx<16>(f.tbase, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
+        ephdc_tmem::ldx<16>(f.tbase + 16u, *reinterpret_cast<uint32_t(*)[16]>(&rr[16]));
+        ephdc_tmem::ldx<16>(f.tbase + 32u, sc[0]);
         double x[16];
         const int st = sw(f.tid);
 #pragma unroll
         for (int k = 0; k < 16; ++k) x[k] = C[st ^ sw(NT * k)];
-        {
-            uint32_t rr[32];
-            ephdc_tmem::ldx<16>(f.tbase, *reinterpret_cast<uint32_t(*)[16]>(&rr[0]));
-            ephdc_tmem::ldx<16>(f.tbase + 16u, *reinterpret_cast<uint32_t(*)[16]>(&rr[16]));
-            ephdc_tmem::waitx<32>(rr);
-            dit_stages<4, 0, 3>(x, [&](int sub, int kk) { return pair_at(rr, (1 << sub) - 1 + kk); }, f.nq);
-        }
+        ephdc_tmem::waitx<32>(rr);
+        ephdc_tmem::waitx<16>(sc[0]);
+        dit_stages<4, 0, 3>(x, [&](int sub, int kk) { return pair_at(rr, (1 << sub) - 1 + kk); }, f.nq);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            uint32_t rr[16];
-            ephdc_tmem::ldx<16>(f.tbase + 32u + 16u * h, rr);
-            ephdc_tmem::waitx<16>(rr);
+            if (h < 3) ephdc_tmem::ldx<16>(f.tbase + 32u + 16u * (h + 1), sc[(h + 1) & 1]);
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 const int k = 2 * h + v;
-                const double2 sj = pair_at(rr, 2 * v), swj = pair_at(rr, 2 * v + 1);
+                const double2 sj = pair_at(sc[h & 1], 2 * v), swj = pair_at(sc[h & 1], 2 * v + 1);
                 const double A = mul_tw(x[k], sj.x, sj.y, f.nq), Bv = mul_tw(x[k + 8], swj.x, swj.y, f.nq);
                 sink(k, __dadd_rn(A, Bv));
                 sink(k + 8, mul_tw(__dsub_rn(A, Bv), cloc.x, cloc.y, f.nq));
             }
+            if (h < 3) ephdc_tmem::waitx<16>(sc[(h + 1) & 1]);
         }
     }
 };
@@ -616,9 +726,7 @@ __global__ void __launch_bounds__((1 << LGC) / kE, ctas_per_sm<LGC>())
             const double2 *twg = a.tw + (size_t)j * NC, *tl = a.tail + (size_t)j * NC;
             I::load_twiddles(f, [&](int p) { return twg[p]; }, [&](int p) { return tl[p]; });
             ephdc_tmem::wait_st();
-            f.q = twg[0].x;
-            f.nq = -f.q;
-            f.qinv = twg[0].y;
+            f.set_prime(twg[0]);
             cloc = a.cinv[j];
             jcur = j;
             ephdc_tmem::fence_before_sync();
@@ -633,8 +741,70 @@ __global__ void __launch_bounds__((1 << LGC) / kE, ctas_per_sm<LGC>())
         u64 *o = poly_ptr(a, w);
         I::pass_d(f, C, cloc, [&](int k, double v) {
             __stcs(reinterpret_cast<unsigned long long *>(o + f.tid + NT * k),
-                   (unsigned long long)out_u64(v, f.q, f.nq, f.qinv));
+                   (unsigned long long)out_u64(v, f));
         });
+    }
+    frame_exit<LGC>(f, tmem_slot);
+}
+
+// Inverse with two warp groups (N = 2^13; see k_ntt_c5_fwd2g): passes A-C of both
+// halves (warp-local), the group barrier, pass D of both halves straight to HBM.
+__global__ void __launch_bounds__(512, 1) k_ntt_c5_inv2g(const __grid_constant__ CUtensorMap map,
+                                                        const __grid_constant__ C5Args a) {
+    constexpr int LGC = 13;
+    using I = Inv<LGC>;
+    constexpr int NC = I::NC, NT = I::NT;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar[kNBuf];
+    __shared__ uint32_t tmem_slot;
+    Ctx f;
+    frame_init<LGC>(f, smem_raw, kNBuf, mbar, &tmem_slot);
+    const int g = f.warp >> 3, gt = f.tid & 255;
+    const u32 w0 = (u32)((u64)a.items * blockIdx.x / gridDim.x), w1 = (u32)((u64)a.items * (blockIdx.x + 1) / gridDim.x);
+    const u32 n = w1 - w0;
+    auto issue = [&](u32 i) {
+        uint64_t *bar = &mbar[i % 3];
+        ephdc_async::fence_proxy_async();
+        ephdc_async::mbar_arrive_expect_tx(bar, (u32)(NC * 8));
+        double *c = f.bufs + (size_t)(i % 3) * NC;
+        const int row0 = poly_row(a, w0 + i);
+#pragma unroll
+        for (int r = 0; r < NC / 16; r += kBoxRows) tma_load_2d(c + 16 * r, &map, 0, row0 + r, bar);
+    };
+    if (f.tid == 0)
+        for (u32 i = 0; i < 3 && i < n; ++i) issue(i);
+    for (u32 i0 = 0; i0 < n;) {
+        const u32 i1 = segment_end(a, w0, w1, i0), j = (w0 + i0) / a.batch;
+        __syncthreads();
+        const double2 *twg = a.tw + (size_t)j * NC, *tl = a.tail + (size_t)j * NC;
+        I::load_twiddles(half_ctx(f, g), [&](int p) { return twg[p]; }, [&](int p) { return tl[p]; });
+        ephdc_tmem::wait_st();
+        f.set_prime(twg[0]);
+        const double2 cloc = a.cinv[j];
+        ephdc_tmem::fence_before_sync();
+        __syncthreads();
+        ephdc_tmem::fence_after_sync();
+        const bool pair = i0 + 1 < i1;
+        if (g == 1 && pair) bar_sync(3, 512);
+        for (u32 i = i0 + g; i < i1; i += 2) {
+            ephdc_async::mbar_wait(&mbar[i % 3], (i / 3) & 1u);
+            double *C = f.bufs + (size_t)(i % 3) * NC;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) I::passes_abc(half_ctx(f, h), C);
+            bar_sync(1 + g, 256);
+            if (g == 0 && i == i0 && pair) bar_arrive(3, 512);
+            if (gt == 0 && i >= 2 && i + 1 < n) issue(i + 1);
+            u64 *o = poly_ptr(a, w0 + i);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const Ctx v = half_ctx(f, h);
+                I::pass_d(v, C, cloc, [&](int k, double val) {
+                    __stcs(reinterpret_cast<unsigned long long *>(o + v.tid + NT * k),
+                           (unsigned long long)out_u64(val, v));
+                });
+            }
+        }
+        i0 = i1;
     }
     frame_exit<LGC>(f, tmem_slot);
 }
@@ -703,9 +873,7 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_inv_cl(const __grid_constant_
             }
             if (f.tid < C) ck[f.tid] = a.ck[j * 8 + f.tid];
             ephdc_tmem::wait_st();
-            f.q = twg[0].x;
-            f.nq = -f.q;
-            f.qinv = twg[0].y;
+            f.set_prime(twg[0]);
             cloc = a.cinv[j];
             jcur = j;
             ephdc_tmem::fence_before_sync();
@@ -744,7 +912,7 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_inv_cl(const __grid_constant_
             for (int k = 0; k < C; ++k) {
                 const double y = k == 0 ? x[0] : mul_tw(x[k], ck[k].x, ck[k].y, f.nq);
                 __stcs(reinterpret_cast<unsigned long long *>(o + r + NC * k),
-                       (unsigned long long)out_u64(y, f.q, f.nq, f.qinv));
+                       (unsigned long long)out_u64(y, f));
             }
         }
     }
@@ -948,7 +1116,10 @@ cudaError_t launch_ntt_c5(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t 
     if (inverse) {
         switch (pl->log2N) {
             case 12: return c5_launch(k_ntt_c5_inv<12>, s12, 1, 2, 256, pl, d_polys, batch, true, 256, st);
-            case 13: return c5_launch(k_ntt_c5_inv<13>, s13, 1, 1, 512, pl, d_polys, batch, true, 256, st);
+            case 13:
+                // one team (r16: inverse 0.525 vs 0.502 of HBM with two groups at 48-bit primes)
+                return pl->c5_alt_teams ? c5_launch(k_ntt_c5_inv2g, s13, 1, 1, 512, pl, d_polys, batch, true, 256, st)
+                                        : c5_launch(k_ntt_c5_inv<13>, s13, 1, 1, 512, pl, d_polys, batch, true, 256, st);
             case 14: return c5_launch(k_ntt_c5_inv_cl<2>, s13, 2, 1, 512, pl, d_polys, batch, true, 256, st);
             case 15: return c5_launch(k_ntt_c5_inv_cl<4>, s13, 4, 1, 512, pl, d_polys, batch, true, 256, st);
             case 16: return c5_launch(k_ntt_c5_inv_cl<8>, s13, 8, 1, 512, pl, d_polys, batch, true, 256, st);
@@ -956,7 +1127,10 @@ cudaError_t launch_ntt_c5(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t 
     } else {
         switch (pl->log2N) {
             case 12: return c5_launch(k_ntt_c5_fwd<12>, s12, 1, 2, 256, pl, d_polys, batch, false, 256, st);
-            case 13: return c5_launch(k_ntt_c5_fwd<13>, s13, 1, 1, 512, pl, d_polys, batch, false, 256, st);
+            case 13:
+                // two groups (r16: forward 0.533 vs 0.495 of HBM with one team at 48-bit primes)
+                return pl->c5_alt_teams ? c5_launch(k_ntt_c5_fwd<13>, s13, 1, 1, 512, pl, d_polys, batch, false, 256, st)
+                                        : c5_launch(k_ntt_c5_fwd2g, s13, 1, 1, 512, pl, d_polys, batch, false, 256, st);
             case 14:
                 return pl->c5_red ? c5_launch(k_ntt_c5_fwd_cl<2, true>, s13, 2, 1, 512, pl, d_polys, batch, false, 256, st)
                                   : c5_launch(k_ntt_c5_fwd_cl<2, false>, s13, 2, 1, 512, pl, d_polys, batch, false, 256, st);

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default="", help="lg:L:bits:wordbytes[,...]")
     ap.add_argument("--max-batch-only", action="store_true", help="time only the largest batch of each point")
+    ap.add_argument("--alt-teams", action="store_true", help="A/B: the other warp layout of the c5 kernels at N = 2^13")
     a = ap.parse_args()
     import torch
     import ephdc_inputs as inp
@@ -63,7 +64,7 @@ def main():
             continue
         N = 1 << lg
         q = eph.find_ntt_primes(lg, [bits] * L)
-        plan = eph.NttPlan(q, lg)
+        plan = eph.NttPlan(q, lg, alt_teams=a.alt_teams)
         if wb == 4 and not plan.u32_words:
             continue
         fwd, inv, mac = (eph.ntt_fwd, eph.ntt_inv, eph.mac) if wb == 8 else (eph.ntt_fwd32, eph.ntt_inv32, eph.mac32)
@@ -85,7 +86,7 @@ def main():
             res["clocks"] = clk.stop()
             res["kernels"] = {"fwd": plan.fwd_kernel if wb == 8 else "int_u32",
                               "inv": plan.inv_kernel if wb == 8 else "int_u32"}
-            print(json.dumps({"workload": "c5", "log2N": lg, "L": L, "bits": bits, "word_bits": 8 * wb,
+            print(json.dumps({"workload": "c5", "log2N": lg, "alt_teams": a.alt_teams, "L": L, "bits": bits, "word_bits": 8 * wb,
                               "batch": batch, "bytes_per_launch": 2 * batch * per_poly, "hbm_peak_gbs": hbm,
                               **res}), flush=True)
         del base

@@ -23,13 +23,14 @@ def main():
     ap.add_argument("--op", default="fwd", choices=["fwd", "inv", "mac"])
     ap.add_argument("--batch", type=int, default=0, help="polynomials (0: a 2 GiB working set)")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--alt-teams", action="store_true")
     a = ap.parse_args()
     import torch
     import paper_2511_00737_b200 as eph
 
     N = 1 << a.lg
     q = eph.find_ntt_primes(a.lg, [a.bits] * a.L)
-    plan = eph.NttPlan(q, a.lg)
+    plan = eph.NttPlan(q, a.lg, alt_teams=a.alt_teams)
     per_poly = a.L * N * 8
     dev = torch.device("cuda", 0)
     qt = torch.tensor(q, dtype=torch.int64, device=dev)
