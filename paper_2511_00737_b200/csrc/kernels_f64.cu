@@ -284,6 +284,209 @@ __global__ void __launch_bounds__(mac_threads<LGC, E>(), mac_min_blocks<LGC, E>(
     if (warp == 0) ephdc_tmem::dealloc(tmem_slot, kCols);
 }
 
+// ---------------------------------------------------------------------------------
+// Two warp groups (NC = 2^13: c3, c4).  One CTA per work item as above, but its 16 warps
+// form two 8-warp groups that take alternate dims of the chunk, each with its own NTT
+// buffer (the TMA staging of the plaintext row is dropped: pass 1 reads the row from
+// L2 directly, which frees the 64 KB).  Why: with one team every warp reaches the
+// shared-memory phases of a pass together (barriers align them), so the ~3.5K clocks of
+// shared-memory traffic per dim and the ~9.6K clocks of FP64 work serialise (measured
+// 13.6K per dim); with the groups a pass apart, one group's loads and stores overlap the
+// other's butterflies (the c5 forward gained 8% this way).  Each thread performs the
+// one-team threads vt = t and t + 256 (same registers, same TMEM columns: warps w and
+// w + 8 share a lane quarter), so both groups accumulate into the SAME TMEM accumulators;
+// the read-modify-write of half h is serialised between the groups in dim order by a
+// token per half (named barriers 4 + 2h: group 0 released it, 5 + 2h: group 1 did).
+// ---------------------------------------------------------------------------------
+EPHDC_D void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+EPHDC_D void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int S> constexpr size_t mac_f64_2g_smem() {
+    constexpr size_t nc = (size_t)1 << 13;
+    return sizeof(double2) * (nc / 2) + 2 * sizeof(double) * (size_t)ephdc_f64::padded_len((int)nc);
+}
+
+template <int S>
+__global__ void __launch_bounds__(512, 1)
+    k_ntt_mac_f64_2g(const u32 *__restrict__ M, const double *__restrict__ model, u64 *__restrict__ out, F64MacArgs a) {
+    constexpr int LGC = 13, E = kE, NC = 1 << LGC, N = NC * S, NT = NC / E;
+    constexpr int NBLK = E / 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ uint32_t tmem_slot;
+    double2 *tw = reinterpret_cast<double2 *>(smem_raw);                                  // [NC/2]
+    const int tid = threadIdx.x, warp = tid >> 5, g = warp >> 3, gt = tid & 255;
+    double *buf = reinterpret_cast<double *>(smem_raw + sizeof(double2) * (NC / 2)) + (size_t)g * padded_len(NC);
+    u32 x = blockIdx.x;
+    const u32 bl = x % a.bg;
+    x /= a.bg;
+    const u32 s = x % S;
+    x /= S;
+    const u32 j = x % a.L;
+    x /= a.L;
+    const u32 chunk = x % a.chunks, grp = x / a.chunks;
+    const u32 b = grp * a.bg + bl;
+    if (b >= a.nb) return;
+    const u32 d0 = chunk * a.G, d1 = min(a.D, d0 + a.G);
+    if (d0 >= d1) return;
+    const u32 *Mb = M + (size_t)b * a.D * N;
+    if (warp == 0) ephdc_tmem::alloc(&tmem_slot, 512u);
+    const double2 *twg = a.tw + (size_t)j * N;
+    const double2 qq = twg[0];
+    const double q = qq.x, nq = -q, qinv = qq.y;
+    load_twiddles<LGC, S, E>(tw, twg, (int)s, NC / 2);
+    double2 w1 = make_double2(0.0, 0.0);
+    if constexpr (S > 1) w1 = twg[1];
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    // TMEM of one-team warp vw: accumulators at 128 (vw >> 2) + [0, 64), last-stage
+    // twiddles at + [64, 96), lanes of quarter vw & 3 (= this warp's quarter)
+    auto tacc_of = [&](int vw) {
+        return tmem_slot + ((uint32_t)(32 * (vw & 3)) << 16) + (uint32_t)(vw >> 2) * 128u;
+    };
+    {   // each physical warp w initialises one-team warp w's columns (thread vt = tid)
+        const uint32_t tacc = tacc_of(warp), ttw = tacc + 4u * E;
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll
+        for (int c = 0; c < NBLK; ++c) ephdc_tmem::st16(tacc + 16 * c, z);
+#pragma unroll
+        for (int h = 0; h < E / 8; ++h) {
+            uint32_t t[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double2 w = twg[tail_twiddle_index<LGC, S>((int)s, tail_pair_vt<LGC>(4 * h + k, tid))];
+                t[4 * k] = (uint32_t)__double2loint(w.x);
+                t[4 * k + 1] = (uint32_t)__double2hiint(w.x);
+                t[4 * k + 2] = (uint32_t)__double2loint(w.y);
+                t[4 * k + 3] = (uint32_t)__double2hiint(w.y);
+            }
+            ephdc_tmem::st16(ttw + 16 * h, t);
+        }
+        ephdc_tmem::wait_st();
+    }
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    const uint64_t pol = l2_evict_last_policy();
+    const bool pair = d0 + 1 < d1;
+    if (g == 1 && pair) nbar_sync(3, 512);   // group 1 starts one pass behind group 0
+    for (u32 d = d0 + (u32)g; d < d1; d += 2) {
+        const u32 *row = Mb + (size_t)d * N;
+        const double *c0 = model + (((size_t)d * a.L + j) * 2) * N + (size_t)s * NC;
+        const double *c1 = c0 + N;
+        auto load = [&](int pos) -> double {
+            const double U = from_i32((int)__ldg(row + pos));
+            if constexpr (S == 1) {
+                return U;
+            } else {
+                const double V = from_i32((int)__ldg(row + pos + NC));
+                const double T = mul_tw(V, w1.x, w1.y, nq);
+                return s == 0 ? __dadd_rn(U, T) : __dsub_rn(U, T);
+            }
+        };
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) fwd_pass_vt<LGC, 12, 4, true>(buf, load, tw, nq, gt + 256 * h);
+        nbar_sync(1 + g, 256);
+        if (g == 0 && d == d0 && pair) nbar_arrive(3, 512);
+        const bool red = (d - d0 + 1) % a.red_every == 0;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int vt = gt + 256 * h, vw = vt >> 5;
+            fwd_pass_vt<LGC, 8, 4, false>(buf, load, tw, nq, vt);
+            __syncwarp();
+            double2 mc[4][4];
+            auto load_block = [&](int c, double2 (&dst)[4]) {
+#pragma unroll
+                for (int uu = 0; uu < 2; ++uu) {
+                    const int p = tail_pair_vt<LGC>(2 * c + uu, vt);
+                    dst[2 * uu] = ld_pair(c0 + 2 * p, pol);
+                    dst[2 * uu + 1] = ld_pair(c1 + 2 * p, pol);
+                }
+            };
+#pragma unroll
+            for (int c = 0; c < 2; ++c) load_block(c, mc[c]);
+            fwd_pass_vt<LGC, 4, 4, false>(buf, load, tw, nq, vt);
+            __syncwarp();
+            // the token of half h: dims alternate between the groups
+            if (g == 0 ? d >= d0 + 2 : true) nbar_sync(4 + 2 * h + (g == 0 ? 1 : 0), 512);
+            ephdc_tmem::fence_after_sync();
+            const uint32_t tacc = tacc_of(vw), ttw = tacc + 4u * E;
+#pragma unroll
+            for (int c = 2; c < 4; ++c) load_block(c, mc[c]);
+#pragma unroll
+            for (int c = 0; c < NBLK; ++c) {
+                uint32_t r[16], t[8];
+                ephdc_tmem::ld16(tacc + 16 * c, r);
+                ephdc_tmem::ld8(ttw + 8 * c, t);
+                ephdc_tmem::wait_ld(r);
+                ephdc_tmem::after_wait(t);
+#pragma unroll
+                for (int uu = 0; uu < 2; ++uu) {
+                    const int p = tail_pair_vt<LGC>(2 * c + uu, vt);
+                    const int ad = pad(2 * p);
+                    double x0 = buf[ad], x1 = buf[ad + 1];
+                    ct_bfly(x0, x1, __hiloint2double(t[4 * uu + 1], t[4 * uu]), __hiloint2double(t[4 * uu + 3], t[4 * uu + 2]),
+                            nq);
+                    const double2 m0v = mc[c][2 * uu], m1v = mc[c][2 * uu + 1];
+                    uint32_t *w = &r[uu * 8];
+                    double v[4] = {__hiloint2double(w[1], w[0]), __hiloint2double(w[3], w[2]),
+                                   __hiloint2double(w[5], w[4]), __hiloint2double(w[7], w[6])};
+                    v[0] = __dadd_rn(v[0], mul_rt(m0v.x, x0, qinv, nq));
+                    v[1] = __dadd_rn(v[1], mul_rt(m0v.y, x1, qinv, nq));
+                    v[2] = __dadd_rn(v[2], mul_rt(m1v.x, x0, qinv, nq));
+                    v[3] = __dadd_rn(v[3], mul_rt(m1v.y, x1, qinv, nq));
+                    if (red) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) v[e] = reduce(v[e], qinv, nq);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        w[2 * e] = (uint32_t)__double2loint(v[e]);
+                        w[2 * e + 1] = (uint32_t)__double2hiint(v[e]);
+                    }
+                }
+                ephdc_tmem::st16(tacc + 16 * c, r);
+            }
+            ephdc_tmem::wait_st();
+            ephdc_tmem::fence_before_sync();
+            if (d + 1 < d1) nbar_arrive(4 + 2 * h + (g == 0 ? 0 : 1), 512);   // pass the token on
+        }
+        nbar_sync(1 + g, 256);   // the next dim's first pass overwrites buf
+    }
+    // fold: each physical warp w folds one-team warp w's accumulators
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    {
+        const uint32_t tacc = tacc_of(warp);
+        uint32_t r[NBLK][16];
+#pragma unroll
+        for (int c = 0; c < NBLK; ++c) ephdc_tmem::ld16(tacc + 16 * c, r[c]);
+        ephdc_tmem::wait_ld(r[0]);
+#pragma unroll
+        for (int c = 1; c < NBLK; ++c) ephdc_tmem::after_wait(r[c]);
+        u64 *o0 = out + (((size_t)b * 2 + 0) * a.L + j) * N + (size_t)s * NC;
+        u64 *o1 = out + (((size_t)b * 2 + 1) * a.L + j) * N + (size_t)s * NC;
+#pragma unroll
+        for (int u = 0; u < E / 2; ++u) {
+            const int p = tail_pair_vt<LGC>(u, tid);
+            const uint32_t *w = &r[u >> 1][(u & 1) * 8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double v = reduce(__hiloint2double(w[2 * e + 1], w[2 * e]), qinv, nq);
+                u64 *o = (e < 2 ? o0 : o1) + 2 * p + (e & 1);
+                atomicAdd(reinterpret_cast<unsigned long long *>(o), (unsigned long long)to_canonical_u64(v, q));
+            }
+        }
+    }
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    if (warp == 0) ephdc_tmem::dealloc(tmem_slot, 512u);
+}
+
 // Plaintext NTTs for the parity export: p_hat[dd][j] = NTT_j(lift(M[dd])), canonical.
 // CTA = (dim dd, prime j, slice s); same passes as the fused kernel.
 template <int LGC, int S>
@@ -664,7 +867,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     // keep WL = 1 with the prefetch (c2: WL = 2 is 20% slower).
     // ephdc_plan.flags (workspace plan overrides, tests/profiling): bits 1-2 = 1/2/3 force
     // WL = 0/2/1; bit 0 forces the prefetch off, bit 4 on; bit 3 = 32 elements per
-    // thread (LGC = 13 only; WL = 2 or 1).
+    // thread (LGC = 13 only; WL = 2 or 1); bit 5 = the one-team kernel at LGC = 13.
     const u32 env = plan.flags;
     u32 wl = LGC >= 13 ? 2u : 1u;
     bool prefetch = LGC < 13;
@@ -677,6 +880,31 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     if (env & 1u) prefetch = false;
     if (env & 16u) prefetch = true;
     const bool e32 = LGC == 13 && (env & 8u) != 0;
+    // NC = 2^13 (c3, c4): the two-group kernel unless the plan asks for a one-team
+    // variant (flags bits 1-3, or bit 5 = the one-team kernel with the default plan)
+    if constexpr (LGC == 13) {
+        if (!dlim && (env & (32u | 14u)) == 0) {
+            auto k2 = k_ntt_mac_f64_2g<S>;
+            const size_t smem2 = mac_f64_2g_smem<S>();
+            cudaError_t e2 = smem_attr(k2, smem2);
+            if (e2 != cudaSuccess) return e2;
+            F64MacArgs a = f64_args(c);
+            a.nb = nb;
+            f64_grid(c, nb, &a.bg, &a.chunks, &a.G);
+            a.flags = 1u;
+            if (plan.bg) a.bg = std::max<u32>(1, std::min<u32>(nb, plan.bg));
+            if (plan.G) {
+                const u32 gmin = (c->p.D_live + 1023) / 1024;
+                a.G = std::max<u32>(gmin, std::min<u32>(c->p.D_live, plan.G));
+                a.chunks = (c->p.D_live + a.G - 1) / a.G;
+            }
+            const uint64_t groups = (nb + a.bg - 1) / a.bg;
+            const uint64_t grid = groups * a.chunks * a.bg * c->L * S;
+            if (grid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+            k2<<<(unsigned)grid, 512, smem2, st>>>(M, model, out, a);
+            return counted(cudaGetLastError());
+        }
+    }
     auto kern = dlim ? (wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE, true> : k_ntt_mac_f64<LGC, S, 1, kE, true>)
                 : e32 ? (wl == 2 ? k_ntt_mac_f64<LGC, S, 2, 32> : k_ntt_mac_f64<LGC, S, 1, 32>)
                       : wl == 0 ? k_ntt_mac_f64<LGC, S, 0, kE> : wl == 2 ? k_ntt_mac_f64<LGC, S, 2, kE> : k_ntt_mac_f64<LGC, S, 1, kE>;

@@ -159,6 +159,50 @@ EPHDC_D void fwd_ntt_tail(const double *buf, int u, double w, double wq, double 
 }
 
 // ---------------------------------------------------------------------------------
+// The same passes for an explicit thread index vt (the two-group fused kernel: each
+// thread of an 8-warp group performs the one-team threads vt = t and t + 256 in turn).
+// Separate functions on purpose: the one-team kernel's schedule is sensitive to any
+// change of its code (kernels_f64.cu, PREFIX).
+// ---------------------------------------------------------------------------------
+template <int LGC, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+EPHDC_D void fwd_pass_vt(double *buf, const Load &load, const double2 *tw, double nq, int vt) {
+    constexpr int R = 1 << R_LOG;
+    constexpr int TL_LOG = T0_LOG - (R_LOG - 1);
+    constexpr int TL = 1 << TL_LOG;
+    const int g = vt;
+    const int blk = g >> TL_LOG, off = g & (TL - 1);
+    const int base = (blk << (T0_LOG + 1)) + off;
+    constexpr bool kConstPad = T0_LOG >= 3;
+    const int pb = pad(base);
+    auto addr = [&](int k) { return kConstPad ? pb + k * TL + ((k * TL) >> 4) : pad(base + k * TL); };
+    double x[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
+        else x[k] = buf[addr(k)];
+    }
+    constexpr int m0 = (1 << LGC) >> (T0_LOG + 1);
+#pragma unroll
+    for (int sub = 0; sub < R_LOG; ++sub) {
+        const int h = R >> (sub + 1);
+#pragma unroll
+        for (int v = 0; v < (1 << sub); ++v) {
+            const double2 w = tw[(m0 << sub) + v * m0 + blk];
+#pragma unroll
+            for (int kk = 0; kk < h; ++kk) ct_bfly(x[v * 2 * h + kk], x[v * 2 * h + kk + h], w.x, w.y, nq);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) buf[addr(k)] = x[k];
+}
+
+// windowed last-stage pair (tail_pair<LGC, true>) of one-team thread vt
+template <int LGC> EPHDC_D int tail_pair_vt(int u, int vt) {
+    constexpr int NT = (1 << LGC) / kE;
+    return (u >> 3) * (8 * NT) + (vt >> 5) * 256 + (vt & 31) + 32 * (u & 7);
+}
+
+// ---------------------------------------------------------------------------------
 // Inverse (Gentleman-Sande) passes on doubles, for the standalone c5 transform.  The
 // sums X + Y double their bound every stage, so callers check 2^(LGC-1) * B0 < 2^51
 // (ephdc_ntt_plan_create).  Twiddles in shared memory in the pass-major layout: the

@@ -107,16 +107,19 @@ def test_ntt_c5_prime_switch(log2N, L, bits, batch):
     assert np.array_equal(_host(d), x)
 
 
-@pytest.mark.parametrize("batch", [1, 2, 3, 7, 301])
-def test_ntt_c5_two_groups_equal_one_team(batch):
-    """N = 2^13: the two-group kernels (alternate polynomials, group barriers, segment per
-    prime, the TMA ring advanced by the group that frees a buffer) = the one-team kernels,
-    bit for bit, both directions (default forward = two groups, inverse = one team;
-    EPHDC_NTT_ALT_TEAMS swaps), at odd batch sizes (a group with no item, one-item segments)."""
-    N, L = 1 << 13, 3
-    q = nt.prime_chain([48] * L, 13)
-    x = inp.gen_residues(q, batch, N, seed=77 + batch)
-    p2, p1 = eph.NttPlan(q, 13), eph.NttPlan(q, 13, alt_teams=True)
+@pytest.mark.parametrize("log2N,batch", [(13, 1), (13, 2), (13, 3), (13, 7), (13, 301), (14, 1), (14, 2), (14, 5),
+                                         (14, 160), (15, 3), (15, 41), (16, 2), (16, 19)])
+def test_ntt_c5_two_groups_equal_one_team(log2N, batch):
+    """The two-group c5 kernels (alternate polynomials, group barriers, a segment per
+    prime, the TMA ring advanced by the group that frees a buffer; on clusters the
+    cross-level outputs pushed by st.async onto the partner's mbarrier, buffer reuse
+    signalled by remote arrives) = the one-team kernels, bit for bit, both directions
+    (EPHDC_NTT_ALT_TEAMS swaps the layouts), at odd batch sizes (a group with no item,
+    one-item segments)."""
+    N, L = 1 << log2N, 3
+    q = nt.prime_chain([48 if log2N <= 14 else 44] * L, log2N)
+    x = inp.gen_residues(q, batch, N, seed=77 + batch + log2N)
+    p2, p1 = eph.NttPlan(q, log2N), eph.NttPlan(q, log2N, alt_teams=True)
     assert p2.fwd_kernel == p1.fwd_kernel == "c5_f64" and p2.inv_kernel == "c5_f64"
     d2, d1 = _dev(x), _dev(x)
     eph.ntt_fwd(p2, d2)
@@ -124,7 +127,7 @@ def test_ntt_c5_two_groups_equal_one_team(batch):
     assert torch.equal(d2, d1)
     b = batch - 1
     psi = nt.min_primitive_2n_root(q[L - 1], N)
-    assert np.array_equal(_host(d2)[b, L - 1], core.ntt_fwd(x[b, L - 1][None, :], 13, q[L - 1], psi)[0])
+    assert np.array_equal(_host(d2)[b, L - 1], core.ntt_fwd(x[b, L - 1][None, :], log2N, q[L - 1], psi)[0])
     eph.ntt_inv(p2, d2)
     eph.ntt_inv(p1, d1)
     assert torch.equal(d2, d1)

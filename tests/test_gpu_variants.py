@@ -3,7 +3,8 @@
 The default plan (f64_grid + the WL / prefetch choice in mac_f64_launch) is checked
 against the oracle by test_gpu_fullsize / test_gpu_parity; every other variant the
 workspace plan overrides (ephdc_plan) select must produce exactly the same scores ciphertexts:
-the synchronisation variants WL = 0/1/2, 32 elements per thread, the explicit L2
+the two-group kernel (the NC = 2^13 default) against the one-team kernel, the
+synchronisation variants WL = 0/1/2, 32 elements per thread, the explicit L2
 prefetch on/off, and other grid plans (batches per group, dims per chunk -- i.e. other
 orders of the 64-bit atomic folds, which integer addition makes order independent).
 Each variant's output also decrypts to the brute-force integer scores.
@@ -32,8 +33,11 @@ VARIANTS = [
     {"flags": 8},            # 32 elements per thread (NC = 2^13 only), planned WL
     {"flags": 14},           # 32 elements per thread, WL = 1
     {"flags": 12},           # 32 elements per thread, WL = 2
-    {"bg": 1, "G": 37},
+    {"flags": 32},           # the one-team kernel (default plan) at NC = 2^13
+    {"bg": 1, "G": 37},      # (two groups) odd chunks: the groups' dims and tokens
     {"bg": 2, "G": 1000},
+    {"bg": 3, "G": 9},       # chunks of 9 dims (the planner's minimum at c3 is 8)
+    {"flags": 32, "G": 37},
 ]
 
 

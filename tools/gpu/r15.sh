@@ -1,5 +1,6 @@
 # measurement hygiene run: every config's bench line (clocks, cpu_baseline all cores), the
 # single-core oracle for c1q3-c3, the oracle reference arm at c4, SR with clocks, c5 sweep
+timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q > gpurun_out/r15/pytest_k.log 2>&1; tail -n 2 gpurun_out/r15/pytest_k.log
 mkdir -p gpurun_out/r15
 for c in c1q3 c2 c3 c4; do
   timeout 900 python bench.py --config $c > gpurun_out/r15/bench_$c.json 2> gpurun_out/r15/bench_$c.err
