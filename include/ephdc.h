@@ -113,8 +113,9 @@ typedef struct {
                           * synchronisation WL = 0/2/1; bit 0 = no L2 prefetch of the
                           * model slice, bit 4 = prefetch; bit 3 = 32 elements per
                           * thread (NC = 2^13); bit 5 = the one-team kernel at NC =
-                          * 2^13 (default: two warp groups; bits 1-3 also select a
-                          * one-team variant)                                         */
+                          * 2^13 with one slice (default there: two warp groups; bits
+                          * 1-3 also select a one-team variant); bit 6 = the two-group
+                          * kernel at N = 2^14 (default there: one team)              */
     uint32_t bg;         /* FP64 fused kernel: batches per group (0 = planner)       */
     uint32_t G;          /* FP64 fused kernel: dims per chunk (0 = planner)          */
     uint32_t m_batches;  /* batches of encoded plaintexts kept (0 = planner: all of

@@ -868,7 +868,7 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     // ephdc_plan.flags (workspace plan overrides, tests/profiling): bits 1-2 = 1/2/3 force
     // WL = 0/2/1; bit 0 forces the prefetch off, bit 4 on; bit 3 = 32 elements per
     // thread (LGC = 13 only; WL = 2 or 1); bit 5 = the one-team kernel at LGC = 13.
-    const u32 env = plan.flags;
+    u32 env = plan.flags;
     u32 wl = LGC >= 13 ? 2u : 1u;
     bool prefetch = LGC < 13;
     switch ((env >> 1) & 3u) {
@@ -880,9 +880,13 @@ static cudaError_t mac_f64_launch(const ephdc_ctx *c, const ephdc_plan &plan, co
     if (env & 1u) prefetch = false;
     if (env & 16u) prefetch = true;
     const bool e32 = LGC == 13 && (env & 8u) != 0;
-    // NC = 2^13 (c3, c4): the two-group kernel unless the plan asks for a one-team
-    // variant (flags bits 1-3, or bit 5 = the one-team kernel with the default plan)
+    // NC = 2^13, S = 1 (c3): the two-group kernel unless the plan asks for a one-team
+    // variant (flags bits 1-3, or bit 5 = the one-team kernel with the default plan).
+    // At S = 2 (c4) the one-team kernel stays the default: two groups measured 259.6 vs
+    // 246.0 ms per c4 step (c3: 19.45 vs 19.95 ms; profiles/r02/ab/bench_*).  Plan bit 6
+    // selects the two-group kernel at S = 2 (A/B).
     if constexpr (LGC == 13) {
+        if (S == 2 && !(env & 64u)) env |= 32u;
         if (!dlim && (env & (32u | 14u)) == 0) {
             auto k2 = k_ntt_mac_f64_2g<S>;
             const size_t smem2 = mac_f64_2g_smem<S>();

@@ -38,6 +38,8 @@ VARIANTS = [
     {"bg": 2, "G": 1000},
     {"bg": 3, "G": 9},       # chunks of 9 dims (the planner's minimum at c3 is 8)
     {"flags": 32, "G": 37},
+    {"flags": 64},           # the two-group kernel at N = 2^14 (c4; one team by default)
+    {"flags": 64, "bg": 1, "G": 37},
 ]
 
 
