@@ -3,6 +3,7 @@
 // it lowers to is checked with cuobjdump. Reports ops/clk/SM using clock64/globaltimer.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o int_peak int_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -129,7 +130,43 @@ static void run(const char *name, K kern, int blocks, int threads) {
     cudaFree(clk);
 }
 
-int main() {
+// Sustained: the butterfly mix at the c5 kernels' occupancy (one 512-thread CTA per SM)
+// launched back to back for `seconds`, so the clock and power state are those of a long
+// run (an external nvidia-smi sampler records them): the measured FP64 ceiling of the
+// NTT's instruction mix.
+static void sustained(double seconds) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double *out;
+    unsigned long long *clk;
+    cudaMalloc(&out, sizeof(double) * sms * 512);
+    cudaMalloc(&clk, 16);
+    k_bfly<<<sms, 512>>>(out, clk);
+    cudaDeviceSynchronize();
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int launches = 0;
+    float ms = 0.f;
+    cudaEventRecord(a);
+    while (ms < seconds * 1e3) {
+        for (int i = 0; i < 64; ++i) k_bfly<<<sms, 512>>>(out, clk);
+        launches += 64;
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+    }
+    const double ops = (double)launches * sms * 512 * ITERS * CH;
+    printf("{\"op\": \"FP64 butterfly mix sustained (1x512 thr/SM)\", \"Gops\": %.1f, \"seconds\": %.2f, "
+           "\"launches\": %d}\n",
+           ops / (ms * 1e-3) / 1e9, ms * 1e-3, launches);
+}
+
+int main(int argc, char **argv) {
+    if (argc > 2 && argv[1][0] == 's') {   // int_peak sustained <seconds>
+        sustained(atof(argv[2]));
+        return 0;
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int blocks = sms * 8, threads = 256;
