@@ -618,7 +618,10 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
     using F = Fwd<LGC>;
     constexpr int NC = F::NC, NT = F::NT, SL = NC / C, RP = SL / NT;
     extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t mbar[kNBuf];          // [0] = staging (TMA)
+    // the staging buffer's TMA completes on mbar[i & 1] (item i): with ONE barrier, a
+    // group waiting for item i + 1 while item i's copy is still in flight would match
+    // the parity of the previous phase and proceed early (r19: a launch failure)
+    __shared__ __align__(8) uint64_t mbar[kNBuf];
     __shared__ __align__(8) uint64_t full[2], empty[2];    // per group
     __shared__ uint32_t tmem_slot;
     __shared__ double2 xtw[8];
@@ -638,12 +641,13 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
     const u32 s = cluster_rank(), unit = blockIdx.x / C, nunits = gridDim.x / C;
     const u32 w0 = (u32)((u64)a.items * unit / nunits), w1 = (u32)((u64)a.items * (unit + 1) / nunits);
     const u32 n = w1 - w0;
-    auto issue = [&](u32 i) {   // one thread; the staging buffer (mbarrier 0)
+    auto issue = [&](u32 i) {   // one thread; the staging buffer
+        uint64_t *bar = &mbar[i & 1u];
         ephdc_async::fence_proxy_async();
-        ephdc_async::mbar_arrive_expect_tx(&mbar[0], (u32)(NC * 8));
+        ephdc_async::mbar_arrive_expect_tx(bar, (u32)(NC * 8));
         const int row0 = poly_row(a, w0 + i);
 #pragma unroll
-        for (int k = 0; k < C; ++k) tma_load_2d(stage + k * SL, &map, 0, row0 + ((k * NC + (int)s * SL) >> 4), &mbar[0]);
+        for (int k = 0; k < C; ++k) tma_load_2d(stage + k * SL, &map, 0, row0 + ((k * NC + (int)s * SL) >> 4), bar);
     };
     if (f.tid == 0 && n > 0) issue(0);
     u32 ng = 0;   // items this group has processed
@@ -662,7 +666,7 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
         for (u32 i = i0 + g; i < i1; i += 2, ++ng) {
             if (ng > 0) mbar_wait_cluster(&empty[g], (ng - 1) & 1u);   // partners' group-g buffers are free
             if (gt == 0) ephdc_async::mbar_arrive_expect_tx(&full[g], (u32)((C - 1) * SL * 8));
-            mbar_wait_bounded(&mbar[0], i & 1u);
+            mbar_wait_bounded(&mbar[i & 1u], (i >> 1) & 1u);
             // ---- cross levels on the slice: r = s SL + rl, rl = vtid + u NT, elements r + k NC
             const u64 *Su = reinterpret_cast<const u64 *>(stage);
 #pragma unroll 1
