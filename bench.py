@@ -61,6 +61,17 @@ def parse():
     return ap.parse_args()
 
 
+def fp64_ceiling():
+    """The FP64 butterfly mix's sustained rate measured on a B200 (tools/int_peak.cu
+    `sustained`, profiles/r02/r19/fp64_ceiling.json) and this kernel's fraction of it is
+    reported next to the nominal peak; None if the record is absent."""
+    try:
+        rec = json.loads(open(os.path.join(ROOT, "profiles", "r02", "r19", "fp64_ceiling.json")).readline())
+        return {"value": rec["Gops"], "unit": "GFP64op/s", "source": "profiles/r02/r19/fp64_ceiling.json"}
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -297,6 +308,9 @@ def main():
                                 "model_bytes": D * L * 2 * N * 8, "launches_per_step": mac_n / a.steps},
                 "mulmod_rate_G_per_s": round((bfly + macs) / mac_s / 1e9, 1),
                 "peak_source": src,
+                "measured_ceiling": fp64_ceiling() if ctx.arith == "f64" else None,
+                "frac_of_measured_ceiling": (round(achieved / fp64_ceiling()["value"], 4)
+                                             if ctx.arith == "f64" and fp64_ceiling() else None),
                 "share_of_step": round(mac_ms / max(total_ms, 1e-9), 4),
                 "kernel_ms": {k: round(v[0] / a.steps, 3) for k, v in kt.items()}}
 
