@@ -386,10 +386,11 @@ ephdc_status ephdc_noise_probe(const ephdc_ctx *ctx, const ephdc_sk *sk, const u
 /* Tables for L primes (each = 1 mod 2N, < 2^61) at ring degree N = 2^log2N,
  * 10 <= log2N <= 16, on `device`.  flags: 0 = the tuned kernels (FP64 pipe where
  * the bounds of DESIGN.md 5.1 hold, else the integer pipe); EPHDC_NTT_FORCE_INT =
- * the integer-pipe kernels everywhere; EPHDC_NTT_ALT_TEAMS = at N = 2^13 the other
- * warp layout of the c5 kernels (forward: one 16-warp team instead of two 8-warp
- * groups; inverse: two groups instead of one team) (TEST/PROFILING only, both:
- * bit-identical results).
+ * the integer-pipe kernels everywhere; EPHDC_NTT_ALT_TEAMS = the alternative
+ * layouts kept for A/B: at N = 2^13 the other warp layout of the c5 kernels (forward:
+ * one 16-warp team instead of two 8-warp groups; inverse: two groups instead of one
+ * team), at 2^14-2^16 the one-team cluster kernels, and the per-polynomial integer
+ * kernel instead of the persistent one (TEST/PROFILING only, all bit-identical).
  * Synchronous.  Errors: ENULL, EPARAM (sizes, a q_j that is not an NTT prime, unknown
  * flags), ECONTEXT (device < 0), ECUDA, ERESOURCE. */
 #define EPHDC_NTT_FORCE_INT 1u

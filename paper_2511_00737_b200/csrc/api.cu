@@ -991,6 +991,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
     plan_ntt_f64(p->q, log2N, &p->fwd_f64, &p->inv_f64, &p->inv_dit);
     if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
     p->c5_alt_teams = (flags & EPHDC_NTT_ALT_TEAMS) != 0;
+    p->int_per_poly = p->c5_alt_teams;
     // the c5 kernels (ntt_c5.cu) use the FP64 forward table at every N >= 2^12 whose
     // primes are all < 2^50; their own bounds are decided in plan_ntt_c5
     const bool c5_candidate = !(flags & EPHDC_NTT_FORCE_INT) && log2N >= 12 &&

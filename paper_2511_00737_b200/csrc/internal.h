@@ -141,6 +141,7 @@ struct ephdc_ntt_plan {
     // after its cross levels
     bool c5_fwd = false, c5_inv = false, c5_red = false;
     bool c5_alt_teams = false;   // EPHDC_NTT_ALT_TEAMS (A/B only)
+    bool int_per_poly = false;   // EPHDC_NTT_ALT_TEAMS also selects the per-polynomial integer kernel (A/B)
     // inverse: DIT table [L][N] (W[h + jj] = omega^-(N/2h) jj, entry 0 = (q, 1/q)), fused
     // level-12 scaling [L][NC/2][2] (sigma_r, sigma_r W[NC/2 + r]), sigma_r = N^-1 psi^-r;
     // c_loc = psi^-(NC/2); block constants c_k = psi^-(NC k) [L][8]

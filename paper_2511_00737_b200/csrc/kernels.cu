@@ -483,6 +483,72 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>()) k_ntt_batch(W *__re
     }
 }
 
+// Persistent form of k_ntt_batch for one-CTA transforms (S = 1): a CTA walks a
+// contiguous range of (prime, polynomial) items, prime-major, with the prime's whole
+// twiddle table staged in shared memory once (the per-polynomial kernel reads it from
+// L1/L2 in every pass).  u32 words: up to 2^14 (table + buffer 192 KB); u64: up to 2^13.
+template <int LG, bool INV, typename W> constexpr size_t nttp_smem() {
+    return sizeof(TwPair<W>) * ((size_t)1 << LG) + sizeof(W) * (size_t)padded_len(1 << LG);
+}
+template <int LG, typename W> constexpr int nttp_ctas_per_sm() {
+    constexpr int by_smem = (int)((200u << 10) / nttp_smem<LG, false, W>());
+    return by_smem < 1 ? 1 : by_smem > 4 ? 4 : by_smem;
+}
+
+template <int LG, bool INV, typename W>
+__global__ void __launch_bounds__((1 << LG) / batch_E<LG>(), nttp_ctas_per_sm<LG, W>())
+    k_ntt_batch_p(W *__restrict__ polys, NttArgsW<W> a, u32 batch) {
+    constexpr int E = batch_E<LG>();
+    constexpr int NC = 1 << LG, NT = NC / E;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TwPair<W> *tws = reinterpret_cast<TwPair<W> *>(smem_raw);
+    W *buf = reinterpret_cast<W *>(smem_raw + sizeof(TwPair<W>) * NC);
+    const u32 items = batch * a.L;
+    const u32 w0 = (u32)((u64)items * blockIdx.x / gridDim.x), w1 = (u32)((u64)items * (blockIdx.x + 1) / gridDim.x);
+    u32 jcur = 0xffffffffu;
+    W q = 0, ni = 0, nip = 0;
+    for (u32 w = w0; w < w1; ++w) {
+        const u32 j = w / batch, b = w - j * batch;
+        if (j != jcur) {
+            __syncthreads();
+            const TwPair<W> *tw = a.tw + (size_t)j * NC;
+            for (int i = threadIdx.x; i < NC; i += NT) tws[i] = tw[i];
+            q = (W)a.ps.q[j];
+            if constexpr (INV) {
+                ni = a.ninv[2 * j];
+                nip = a.ninv[2 * j + 1];
+            }
+            jcur = j;
+            __syncthreads();
+        }
+        W *p = polys + ((size_t)b * a.L + j) * NC;
+        if constexpr (!INV) {
+            auto load = [&](int pos) -> W { return ld_stream<W>(p + pos); };
+            fwd_ntt<W, LG, E>(buf, load, tws, NC, q);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int pos = threadIdx.x + e * NT;
+                st_stream<W>(p + pos, reduce4<W>(buf[sidx<W>(pos)], q, (W)(2 * q)));
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int pos = threadIdx.x + e * NT;
+                buf[sidx<W>(pos)] = ld_stream<W>(p + pos);
+            }
+            __syncthreads();
+            auto sload = [&](int pos) -> W { return buf[sidx<W>(pos)]; };
+            inv_ntt<W, LG, E>(buf, sload, tws, q, NC);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int pos = threadIdx.x + e * NT;
+                st_stream<W>(p + pos, csub(mul_shoup_lazy<W>(buf[sidx<W>(pos)], ni, nip, q), q));
+            }
+        }
+        __syncthreads();   // the next item's first pass rewrites buf
+    }
+}
+
 // The GS = log2(N) - 14 global stages: forward (CT; first stages, canonical input ->
 // lazy [0, 4q)) or inverse (GS; last stages, lazy [0, 2q) input -> times N^-1,
 // canonical).  Thread = one radix-2^GS group {i + k * N/2^GS}.
@@ -845,6 +911,25 @@ template <typename W> static NttArgsW<W> ntt_args(const ephdc_ntt_plan *p, bool 
 
 template <int LG, bool INV, typename W>
 static cudaError_t nttb_launch(const ephdc_ntt_plan *p, W *polys, u32 batch, cudaStream_t st) {
+    // one-CTA transforms whose twiddle table fits beside the buffer: the persistent form
+    // where it measured faster (r24, fraction of HBM, persistent vs per polynomial):
+    // u32 inverse 2^12 0.401 vs 0.357, 2^13 0.300 vs 0.223, 2^14 0.265 vs 0.245; u32
+    // forward 2^12 0.445 vs 0.430; u64 (60-bit) forward 2^13 0.203 vs 0.194.  Slower and
+    // so not used: u32 forward 2^13 / 2^14 (0.343 / 0.278 vs 0.362 / 0.363 -- one or two
+    // CTAs per SM instead of up to four), u64 2^12 (0.216 vs 0.264).
+    constexpr bool kPersist = sizeof(W) == 4 ? (INV || LG == 12) : (!INV && LG == 13);
+    if constexpr (kPersist && LG >= 12 && nttp_smem<LG, INV, W>() <= (200u << 10)) {
+        if (p->log2N == LG && !p->int_per_poly) {
+            auto kp = k_ntt_batch_p<LG, INV, W>;
+            constexpr size_t sm = nttp_smem<LG, INV, W>();
+            cudaError_t e = set_smem(kp, sm);
+            if (e != cudaSuccess) return e;
+            const uint64_t items = (uint64_t)batch * p->L;
+            const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(items, 148u * nttp_ctas_per_sm<LG, W>()));
+            kp<<<grid, (1 << LG) / batch_E<LG>(), sm, st>>>(polys, ntt_args<W>(p, INV), batch);
+            return counted(cudaGetLastError());
+        }
+    }
     const size_t smem = sizeof(W) * padded_len(1 << LG);
     auto kern = k_ntt_batch<LG, INV, W>;
     cudaError_t e = set_smem(kern, smem);
