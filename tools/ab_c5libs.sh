@@ -22,4 +22,7 @@ for f in sorted(glob.glob(sys.argv[1] + "/*.jsonl")):
         if "ntt_fwd" in r:
             print(os.path.basename(f), r["log2N"], r["batch"], r["ntt_fwd"]["frac_hbm"], r["ntt_inv"]["frac_hbm"],
                   r["clocks"].get("sm_mhz"), r["clocks"].get("reasons"))
+        elif r.get("op") == "mac":
+            print(os.path.basename(f), "mac", r["log2N"], r["L"], r["bits"], r["D"], r["frac_hbm"],
+                  r["clocks"].get("sm_mhz"), r["clocks"].get("reasons"))
 PY

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/r25
+timeout 2400 python -m pytest tests -m gpu -x -q --durations=10 > gpurun_out/r25/pytest_gpu.log 2>&1; tail -n 14 gpurun_out/r25/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r25/smoke.log 2>&1; tail -n 1 gpurun_out/r25/smoke.log
+timeout 600 python bench.py > gpurun_out/r25/bench_c4.json 2> gpurun_out/r25/bench_c4.err; python3 -c "import json; d=json.loads(open('gpurun_out/r25/bench_c4.json').readline()); print(d['value'], d['ms_per_step'], d['clocks'], d['e2e']['value'], d['roofline']['frac'], d['roofline'].get('frac_of_measured_ceiling'))"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r25/launches_c4.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/r25/ncu_launch.log 2>&1; tail -n 2 gpurun_out/r25/ncu_launch.log; wc -l gpurun_out/r25/launches_c4.csv
+timeout 1800 python tools/bench_c5.py --points all > gpurun_out/r25/c5_all.jsonl 2> gpurun_out/r25/c5_all.err; wc -l gpurun_out/r25/c5_all.jsonl; grep -v "^\s*$" gpurun_out/r25/c5_all.err | tail -n 2
