@@ -11,9 +11,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 
 #include "internal.h"
+#include "modf64.cuh"
 #include "ntt_dev.cuh"
 #include "rng.cuh"
 
@@ -666,6 +668,56 @@ __global__ void __launch_bounds__(256) k_mac(const u64 *__restrict__ ct, const u
     atomicAdd(o + N + 1, a11);
 }
 
+// The same MAC on the FP64 pipe for primes < 2^50 (modf64.cuh: exact products in
+// doubles).  The integer form needs ~12 half/quarter-rate IMAD.WIDE per Montgomery
+// product, about the IMAD.WIDE peak at HBM speed; here a product is 6 FP64 operations
+// (25% of the FP64 pipe at HBM speed).  Accumulators stay below 2^53 by a reduction
+// every red_every terms (red_every (q/2 + 1) < 2^52); sums are true residues (no
+// Montgomery factor): k_mod_q finishes.
+__global__ void __launch_bounds__(256) k_mac_f64(const u64 *__restrict__ ct, const u64 *__restrict__ pt, u32 D, u32 L,
+                                                 u32 N, u32 dsplit, PrimeSet ps, u32 red_every, u64 *__restrict__ out) {
+    using namespace ephdc_f64;
+    const u32 pairs = (L * N) >> 1;
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= pairs) return;
+    const u32 lin = 2 * g, j = lin / N, i = lin % N;
+    const double q = (double)ps.q[j], nq = -q, qinv = 1.0 / q;
+    const u32 per = (D + dsplit - 1) / dsplit;
+    const u32 d0 = blockIdx.y * per, d1 = min(D, d0 + per);
+    double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+    u32 cnt = 0;
+#pragma unroll 4
+    for (u32 d = d0; d < d1; ++d) {
+        const ulonglong2 p = __ldcs(reinterpret_cast<const ulonglong2 *>(pt + ((size_t)d * L + j) * N + i));
+        const ulonglong2 c0 = __ldcs(reinterpret_cast<const ulonglong2 *>(ct + (((size_t)d * L + j) * 2) * N + i));
+        const ulonglong2 c1 = __ldcs(reinterpret_cast<const ulonglong2 *>(ct + (((size_t)d * L + j) * 2 + 1) * N + i));
+        const double px = from_u64(p.x), py = from_u64(p.y);
+        a00 = __dadd_rn(a00, mul_rt(from_u64(c0.x), px, qinv, nq));
+        a01 = __dadd_rn(a01, mul_rt(from_u64(c0.y), py, qinv, nq));
+        a10 = __dadd_rn(a10, mul_rt(from_u64(c1.x), px, qinv, nq));
+        a11 = __dadd_rn(a11, mul_rt(from_u64(c1.y), py, qinv, nq));
+        if (++cnt == red_every) {
+            cnt = 0;
+            a00 = reduce(a00, qinv, nq);
+            a01 = reduce(a01, qinv, nq);
+            a10 = reduce(a10, qinv, nq);
+            a11 = reduce(a11, qinv, nq);
+        }
+    }
+    unsigned long long *o = reinterpret_cast<unsigned long long *>(out + (size_t)j * 2 * N + i);
+    atomicAdd(o, (unsigned long long)to_canonical_u64(reduce(a00, qinv, nq), q));
+    atomicAdd(o + 1, (unsigned long long)to_canonical_u64(reduce(a01, qinv, nq), q));
+    atomicAdd(o + N, (unsigned long long)to_canonical_u64(reduce(a10, qinv, nq), q));
+    atomicAdd(o + N + 1, (unsigned long long)to_canonical_u64(reduce(a11, qinv, nq), q));
+}
+
+// out[i] <- out[i] mod q_j, prime j = (i / N) % L
+__global__ void k_mod_q(u64 *__restrict__ out, u32 L, u32 N, PrimeSet ps, u32 n_total) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_total) return;
+    out[i] %= ps.q[(i / N) % L];
+}
+
 // =====================================================================================
 // launchers
 // =====================================================================================
@@ -1031,11 +1083,19 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
     u32 max_split = (u32)std::min<u64>(~0ull / qmax, 1u << 16);
     u32 dsplit = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
     dsplit = std::min(std::min(dsplit, D), max_split);
+    const u32 n = 2 * L * N;
+    if (qmax < (1ull << 50)) {   // FP64 pipe: 0.96-1.03 of measured HBM vs 0.74-0.77 (r26, profiles/r02/ab)
+        const u32 red_every = (u32)std::max<double>(1.0, std::min<double>(64.0, std::floor(4503599627370496.0 / (double)qmax)));
+        k_mac_f64<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, red_every, d_out);
+        e = counted(cudaGetLastError());
+        if (e != cudaSuccess) return e;
+        k_mod_q<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
+        return counted(cudaGetLastError());
+    }
     k_mac<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, d_out);
     e = counted(cudaGetLastError());
     if (e != cudaSuccess) return e;
     // finalize: output layout [L][2][N]
-    const u32 n = 2 * L * N;
     // reuse k_finalize with the [j][c][i] layout: prime index = i / (2N)
     k_finalize<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
     return counted(cudaGetLastError());

@@ -627,10 +627,26 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
     __shared__ double2 xtw[8];
     Ctx f;
     frame_init<LGC>(f, smem_raw, 3, mbar, &tmem_slot);
+    const u32 s = cluster_rank(), unit = blockIdx.x / C, nunits = gridDim.x / C;
+    const u32 w0 = (u32)((u64)a.items * unit / nunits), w1 = (u32)((u64)a.items * (unit + 1) / nunits);
+    const u32 n = w1 - w0;
+    // items per group (alternate within each prime segment); full[g] is armed for the
+    // group's first item before the start barrier and for its next item right after an
+    // item's last level, BEFORE the partners are told the buffer is free -- so no pushed
+    // byte reaches full[g] ahead of its expect_tx
+    u32 cnt[2] = {0, 0};
+    for (u32 i0 = 0; i0 < n;) {
+        const u32 i1 = segment_end(a, w0, w1, i0);
+        cnt[0] += (i1 - i0 + 1) / 2;
+        cnt[1] += (i1 - i0) / 2;
+        i0 = i1;
+    }
+    const u32 xbytes = (u32)((C - 1) * SL * 8);
     if (f.tid == 0) {
         for (int g = 0; g < 2; ++g) {
             ephdc_async::mbar_init(&full[g], 1);
             ephdc_async::mbar_init(&empty[g], C - 1);
+            if (cnt[g] > 0) ephdc_async::mbar_arrive_expect_tx(&full[g], xbytes);
         }
     }
     cluster_arrive();   // every CTA's barriers are initialised before any remote access
@@ -638,9 +654,6 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
     const int g = f.warp >> 3, gt = f.tid & 255;
     double *stage = f.bufs;
     double *B = f.bufs + (size_t)(1 + g) * NC;               // this group's block buffer
-    const u32 s = cluster_rank(), unit = blockIdx.x / C, nunits = gridDim.x / C;
-    const u32 w0 = (u32)((u64)a.items * unit / nunits), w1 = (u32)((u64)a.items * (unit + 1) / nunits);
-    const u32 n = w1 - w0;
     auto issue = [&](u32 i) {   // one thread; the staging buffer
         uint64_t *bar = &mbar[i & 1u];
         ephdc_async::fence_proxy_async();
@@ -665,7 +678,6 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
         if (g == 1 && pair) bar_sync(3, 512);
         for (u32 i = i0 + g; i < i1; i += 2, ++ng) {
             if (ng > 0) mbar_wait_cluster(&empty[g], (ng - 1) & 1u);   // partners' group-g buffers are free
-            if (gt == 0) ephdc_async::mbar_arrive_expect_tx(&full[g], (u32)((C - 1) * SL * 8));
             mbar_wait_bounded(&mbar[i & 1u], (i >> 1) & 1u);
             // ---- cross levels on the slice: r = s SL + rl, rl = vtid + u NT, elements r + k NC
             const u64 *Su = reinterpret_cast<const u64 *>(stage);
@@ -713,6 +725,7 @@ __global__ void __launch_bounds__(512, 1) k_ntt_c5_fwd_cl2g(const __grid_constan
             }
             bar_sync(1 + g, 256);   // B is read: the partners may write the group's next item
             if (gt == 0) {
+                if (ng + 1 < cnt[g]) ephdc_async::mbar_arrive_expect_tx(&full[g], xbytes);   // before the signal
 #pragma unroll
                 for (int k = 0; k < C; ++k)
                     if (k != (int)s) mbar_remote_arrive(map_rank(&empty[g], (uint32_t)k));
