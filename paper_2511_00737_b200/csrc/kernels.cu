@@ -551,6 +551,123 @@ __global__ void __launch_bounds__((1 << LG) / batch_E<LG>(), nttp_ctas_per_sm<LG
     }
 }
 
+// Two warp groups per CTA for the one-CTA integer transforms at 2^12 / 2^13 (the idea
+// of the c5 FP64 kernels: with one team every warp reaches the load/store phase of a
+// pass together).  Persistent over prime-major items, the prime's twiddle table in
+// shared memory; group g takes alternate items of a prime segment into its own buffer
+// (forward: pass 1 reads the polynomial straight from HBM, coalesced; inverse: a
+// coalesced copy into the buffer first); each thread performs the one-team threads
+// vt = t + 256 h, h < H = NT / 256; group-local named barriers between passes.
+EPHDC_D void gbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+EPHDC_D void gbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int LG, typename W> constexpr size_t ntt2g_smem() {
+    return sizeof(TwPair<W>) * ((size_t)1 << LG) + 2 * sizeof(W) * ((size_t)1 << LG);
+}
+
+template <int LG, bool INV, typename W>
+__global__ void __launch_bounds__(512, 1) k_ntt_batch_2g(W *__restrict__ polys, NttArgsW<W> a, u32 batch) {
+    constexpr int E = kE, NC = 1 << LG, NT = NC / E, H = NT / 256;
+    static_assert(H >= 1 && NT % 256 == 0, "two groups of 256 threads cover the one-team threads");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TwPair<W> *tws = reinterpret_cast<TwPair<W> *>(smem_raw);
+    const int tid = threadIdx.x, g = tid >> 8, gt = tid & 255;
+    W *buf = reinterpret_cast<W *>(smem_raw + sizeof(TwPair<W>) * NC) + (size_t)g * NC;
+    const u32 items = batch * a.L;
+    const u32 w0 = (u32)((u64)items * blockIdx.x / gridDim.x), w1 = (u32)((u64)items * (blockIdx.x + 1) / gridDim.x);
+    auto gsync = [&]() { gbar_sync(1 + g, 256); };
+    for (u32 i0 = w0; i0 < w1;) {
+        const u32 j = i0 / batch, i1 = min(w1, (j + 1) * batch);
+        __syncthreads();
+        const TwPair<W> *tw = a.tw + (size_t)j * NC;
+        for (int i = tid; i < NC; i += 512) tws[i] = tw[i];
+        const W q = (W)a.ps.q[j], two_q = (W)(2 * q);
+        W ni = 0, nip = 0;
+        if constexpr (INV) {
+            ni = a.ninv[2 * j];
+            nip = a.ninv[2 * j + 1];
+        }
+        __syncthreads();
+        const bool pair = i0 + 1 < i1;
+        if (g == 1 && pair) gbar_sync(3, 512);   // group 1 one pass behind
+        for (u32 w = i0 + (u32)g; w < i1; w += 2) {
+            W *p = polys + ((size_t)(w - j * batch) * a.L + j) * NC;
+            if constexpr (!INV) {
+                auto load = [&](int pos) -> W { return ld_stream<W>(p + pos); };
+                // levels in passes of 4 (T0 = LG-1, LG-5, ...), the last pass the remainder
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) fwd_pass_vt<W, LG, E, LG - 1, 4, true>(buf, load, tws, NC, q, two_q, gt + 256 * h);
+                gsync();
+                if (g == 0 && w == i0 && pair) gbar_arrive(3, 512);
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) fwd_pass_vt<W, LG, E, LG - 5, 4, false>(buf, load, tws, NC, q, two_q, gt + 256 * h);
+                gsync();
+                if constexpr (LG - 8 > 4) {   // 2^13: 4 + 4 + 4 + 1
+#pragma unroll 1
+                    for (int h = 0; h < H; ++h) fwd_pass_vt<W, LG, E, LG - 9, 4, false>(buf, load, tws, NC, q, two_q, gt + 256 * h);
+                    gsync();
+#pragma unroll 1
+                    for (int h = 0; h < H; ++h)
+                        fwd_pass_vt<W, LG, E, LG - 13, LG - 12, false>(buf, load, tws, NC, q, two_q, gt + 256 * h);
+                } else {                        // 2^12: 4 + 4 + 4
+#pragma unroll 1
+                    for (int h = 0; h < H; ++h)
+                        fwd_pass_vt<W, LG, E, LG - 9, LG - 8, false>(buf, load, tws, NC, q, two_q, gt + 256 * h);
+                }
+                gsync();
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int pos = gt + 256 * h + e * NT;
+                        st_stream<W>(p + pos, reduce4<W>(buf[sidx<W>(pos)], q, two_q));
+                    }
+                }
+            } else {
+                auto none = [](int) -> W { return 0; };
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int pos = gt + 256 * h + e * NT;
+                        buf[sidx<W>(pos)] = ld_stream<W>(p + pos);
+                    }
+                }
+                gsync();
+                if (g == 0 && w == i0 && pair) gbar_arrive(3, 512);
+                // passes: half-sizes 2^0.., in groups of 4 (DONE = 0, 4, 8, [12])
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) inv_pass_vt<W, LG, E, 0, 4>(buf, none, tws, NC, q, two_q, gt + 256 * h);
+                gsync();
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) inv_pass_vt<W, LG, E, 4, 4>(buf, none, tws, NC, q, two_q, gt + 256 * h);
+                gsync();
+                if constexpr (LG - 8 > 4) {
+#pragma unroll 1
+                    for (int h = 0; h < H; ++h) inv_pass_vt<W, LG, E, 8, 4>(buf, none, tws, NC, q, two_q, gt + 256 * h);
+                    gsync();
+#pragma unroll 1
+                    for (int h = 0; h < H; ++h) inv_pass_vt<W, LG, E, 12, LG - 12>(buf, none, tws, NC, q, two_q, gt + 256 * h);
+                } else {
+#pragma unroll 1
+                    for (int h = 0; h < H; ++h) inv_pass_vt<W, LG, E, 8, LG - 8>(buf, none, tws, NC, q, two_q, gt + 256 * h);
+                }
+                gsync();
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int pos = gt + 256 * h + e * NT;
+                        st_stream<W>(p + pos, csub(mul_shoup_lazy<W>(buf[sidx<W>(pos)], ni, nip, q), q));
+                    }
+                }
+            }
+            gsync();   // the next item's first pass rewrites buf
+        }
+        i0 = i1;
+    }
+}
+
 // The GS = log2(N) - 14 global stages: forward (CT; first stages, canonical input ->
 // lazy [0, 4q)) or inverse (GS; last stages, lazy [0, 2q) input -> times N^-1,
 // canonical).  Thread = one radix-2^GS group {i + k * N/2^GS}.
@@ -969,6 +1086,22 @@ static cudaError_t nttb_launch(const ephdc_ntt_plan *p, W *polys, u32 batch, cud
     // forward 2^12 0.445 vs 0.430; u64 (60-bit) forward 2^13 0.203 vs 0.194.  Slower and
     // so not used: u32 forward 2^13 / 2^14 (0.343 / 0.278 vs 0.362 / 0.363 -- one or two
     // CTAs per SM instead of up to four), u64 2^12 (0.216 vs 0.264).
+    // u32 words: the two-group persistent kernel where it measured fastest (r28, fraction
+    // of HBM, two groups / persistent one team / per polynomial): forward 2^12 0.466 /
+    // 0.445 / 0.424, 2^13 0.365 / 0.343 / 0.361; inverse 2^13 0.328 / 0.300 / 0.224
+    // (inverse 2^12: 0.354 / 0.401 / 0.356 -- the one-team persistent form below)
+    if constexpr (sizeof(W) == 4 && (LG == 13 || (LG == 12 && !INV))) {
+        if (p->log2N == LG && !p->int_per_poly) {
+            auto k2 = k_ntt_batch_2g<LG, INV, W>;
+            constexpr size_t sm2 = ntt2g_smem<LG, W>();
+            cudaError_t e = set_smem(k2, sm2);
+            if (e != cudaSuccess) return e;
+            const uint64_t items = (uint64_t)batch * p->L;
+            const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(items, 148u));
+            k2<<<grid, 512, sm2, st>>>(polys, ntt_args<W>(p, INV), batch);
+            return counted(cudaGetLastError());
+        }
+    }
     constexpr bool kPersist = sizeof(W) == 4 ? (INV || LG == 12) : (!INV && LG == 13);
     if constexpr (kPersist && LG >= 12 && nttp_smem<LG, INV, W>() <= (200u << 10)) {
         if (p->log2N == LG && !p->int_per_poly) {

@@ -165,4 +165,56 @@ EPHDC_D void inv_ntt(W *buf, const Load &load, const TwPair<W> *__restrict__ itw
     inv_passes<W, LG, E, 0, true>(buf, load, itw, tw_num, q, (W)(2 * q));
 }
 
+// ---------------------------------------------------------------------------------
+// The same passes for an explicit one-team thread index vt over NT_ONE = 2^LG / E
+// threads (the two-group kernels: a thread of an 8-warp group performs vt = t and
+// t + 256 in turn); no barrier inside -- the caller synchronises its group.
+// ---------------------------------------------------------------------------------
+template <typename W, int LG, int E, int T0_LOG, int R_LOG, bool FROM_LOAD, class Load>
+EPHDC_D void fwd_pass_vt(W *buf, const Load &load, const TwPair<W> *__restrict__ tw, u32 tw_num, W q, W two_q,
+                         int vt) {
+    constexpr int R = 1 << R_LOG;
+    constexpr int TL_LOG = T0_LOG - (R_LOG - 1);
+    constexpr int TL = 1 << TL_LOG;
+    constexpr int NT = (1 << LG) / E;
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+        const int g = vt + u * NT;
+        const int blk = g >> TL_LOG, off = g & (TL - 1);
+        const int base = (blk << (T0_LOG + 1)) + off;
+        const int sb = sidx_base<W>(base);
+        W x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            if constexpr (FROM_LOAD) x[k] = load(base + k * TL);
+            else x[k] = buf[sidx_at<W>(sb, k * TL)];
+        }
+        const u32 idx0 = (tw_num >> (T0_LOG + 1)) + (u32)blk;
+        ct_substages<W, T0_LOG, R_LOG, 0>(x, tw, idx0, q, two_q);
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[sidx_at<W>(sb, k * TL)] = x[k];
+    }
+}
+
+template <typename W, int LG, int E, int T0_LOG, int R_LOG, class Load>
+EPHDC_D void inv_pass_vt(W *buf, const Load &load, const TwPair<W> *__restrict__ itw, u32 tw_num, W q, W two_q,
+                         int vt) {
+    constexpr int R = 1 << R_LOG;
+    constexpr int T0 = 1 << T0_LOG;
+    constexpr int NT = (1 << LG) / E;
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+        const int g = vt + u * NT;
+        const int blk = g >> T0_LOG, off = g & (T0 - 1);
+        const int base = blk * (T0 * R) + off;
+        const int sb = sidx_base<W>(base);
+        W x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = buf[sidx_at<W>(sb, k * T0)];
+        gs_substages<W, LG, T0_LOG, R_LOG, 0>(x, itw, tw_num, blk, q, two_q);
+#pragma unroll
+        for (int k = 0; k < R; ++k) buf[sidx_at<W>(sb, k * T0)] = x[k];
+    }
+}
+
 }  // namespace ephdc_ntt
