@@ -389,8 +389,8 @@ ephdc_status ephdc_noise_probe(const ephdc_ctx *ctx, const ephdc_sk *sk, const u
  * the integer-pipe kernels everywhere; EPHDC_NTT_ALT_TEAMS = the alternative
  * layouts kept for A/B: at N = 2^13 the other warp layout of the c5 kernels (forward:
  * one 16-warp team instead of two 8-warp groups; inverse: two groups instead of one
- * team), at 2^14-2^16 the one-team cluster kernels, and the per-polynomial integer
- * kernel instead of the persistent one (TEST/PROFILING only, all bit-identical).
+ * team), the one-team cluster forward at 2^14-2^16, and the per-polynomial integer
+ * kernels instead of the persistent ones (TEST/PROFILING only, all bit-identical).
  * Synchronous.  Errors: ENULL, EPARAM (sizes, a q_j that is not an NTT prime, unknown
  * flags), ECONTEXT (device < 0), ECUDA, ERESOURCE. */
 #define EPHDC_NTT_FORCE_INT 1u
@@ -404,7 +404,8 @@ ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t 
 ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream);
 /* Pointwise MAC: d_out[j][c][i] = sum_{d<D} d_ct[d][j][c][i] *
  * d_pt[d][j][i] mod q_j; d_ct [D][L][2][N], d_pt [D][L][N], d_out [L][2][N].
- * Async (the call zeroes d_out itself). */
+ * Exact modular products on the FP64 pipe when every q_j < 2^50, u64 Montgomery
+ * otherwise.  Async (the call zeroes d_out itself). */
 ephdc_status ephdc_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint64_t *d_pt, uint32_t D,
                        uint64_t *d_out, void *stream);
 
