@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define EPHDC_ABI_VERSION 3
+#define EPHDC_ABI_VERSION 4
 #define EPHDC_MAX_PRIMES 16
 
 typedef enum {
@@ -390,11 +390,14 @@ ephdc_status ephdc_noise_probe(const ephdc_ctx *ctx, const ephdc_sk *sk, const u
  * layouts kept for A/B: at N = 2^13 the other warp layout of the c5 kernels (forward:
  * one 16-warp team instead of two 8-warp groups; inverse: two groups instead of one
  * team), the one-team cluster forward at 2^14-2^16, and the per-polynomial integer
- * kernels instead of the persistent ones (TEST/PROFILING only, all bit-identical).
+ * kernels instead of the persistent ones; EPHDC_NTT_U32_GENERIC = the general u32
+ * kernels (kernels.cu) instead of the persistent TMA-fed u32 kernels of ntt32_c5.cu at
+ * N = 2^12 .. 2^14 (TEST/PROFILING only, all bit-identical).
  * Synchronous.  Errors: ENULL, EPARAM (sizes, a q_j that is not an NTT prime, unknown
  * flags), ECONTEXT (device < 0), ECUDA, ERESOURCE. */
 #define EPHDC_NTT_FORCE_INT 1u
 #define EPHDC_NTT_ALT_TEAMS 2u
+#define EPHDC_NTT_U32_GENERIC 4u
 ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N, int device,
                                    uint32_t flags, ephdc_ntt_plan **out);
 void ephdc_ntt_plan_free(ephdc_ntt_plan *p);
@@ -422,9 +425,12 @@ ephdc_status ephdc_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const ui
 #define EPHDC_NTT_KERNEL_INT 0u     /* integer pipe, u64 Shoup (any prime < 2^61)          */
 #define EPHDC_NTT_KERNEL_F64 1u     /* FP64 pipe, per-polynomial CTAs (round-1 kernels)    */
 #define EPHDC_NTT_KERNEL_C5_F64 2u  /* FP64 pipe, persistent TMA-fed kernels (ntt_c5.cu)   */
+#define EPHDC_NTT_KERNEL_C5_U32 3u  /* integer pipe, u32 words, persistent TMA-fed kernels
+                                       (ntt32_c5.cu; N = 2^12 .. 2^14)                   */
 typedef struct {
-    uint32_t fwd_kernel, inv_kernel;  /* EPHDC_NTT_KERNEL_*                               */
+    uint32_t fwd_kernel, inv_kernel;  /* EPHDC_NTT_KERNEL_* of ephdc_ntt_fwd / _inv       */
     uint32_t u32_words;               /* 1 if the *32 entry points are available          */
+    uint32_t u32_kernel;              /* EPHDC_NTT_KERNEL_* of ephdc_ntt_fwd32 / _inv32   */
 } ephdc_ntt_plan_info;
 ephdc_status ephdc_ntt_plan_query(const ephdc_ntt_plan *p, ephdc_ntt_plan_info *info);
 

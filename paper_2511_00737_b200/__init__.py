@@ -424,22 +424,24 @@ def noise_probe(ctx: Context, sk: SecretKey, cts, stream=None) -> Tuple[np.ndarr
 # --------------------------------------------------------------------------- standalone (c5)
 class NttPlan:
     """ephdc_ntt_plan.  force_int: the integer-pipe kernels everywhere (EPHDC_NTT_FORCE_INT);
-    alt_teams: the other warp layout of the c5 kernels at N = 2^13 (EPHDC_NTT_ALT_TEAMS).  Both are
+    alt_teams: the other warp layout of the c5 kernels at N = 2^13 (EPHDC_NTT_ALT_TEAMS); u32_generic:
+    the general u32 kernels instead of the TMA-fed ones of ntt32_c5.cu (EPHDC_NTT_U32_GENERIC).  All are
     tests/profiling switches with bit-identical results."""
 
     def __init__(self, q: Sequence[int], log2N: int, device: int = 0, force_int: bool = False,
-                 alt_teams: bool = False):
+                 alt_teams: bool = False, u32_generic: bool = False):
         self.q = [int(x) for x in q]
         self.L, self.log2N, self.N = len(q), log2N, 1 << log2N
         qa = np.ascontiguousarray(np.array(self.q, dtype=np.uint64))
         self._h = ctypes.c_void_p()
         call("ephdc_ntt_plan_create", _np_ptr(qa), self.L, log2N, device,
-             (1 if force_int else 0) | (2 if alt_teams else 0), ctypes.byref(self._h))
-        info = (ctypes.c_uint32 * 3)()
+             (1 if force_int else 0) | (2 if alt_teams else 0) | (4 if u32_generic else 0), ctypes.byref(self._h))
+        info = (ctypes.c_uint32 * 4)()
         call("ephdc_ntt_plan_query", self._h, ctypes.addressof(info))
-        names = {0: "int", 1: "f64", 2: "c5_f64"}
+        names = {0: "int", 1: "f64", 2: "c5_f64", 3: "c5_u32"}
         self.fwd_kernel, self.inv_kernel = names[info[0]], names[info[1]]
         self.u32_words = bool(info[2])
+        self.u32_kernel = ("int_u32" if info[3] == 0 else names[info[3]]) if self.u32_words else None
 
     @property
     def handle(self):

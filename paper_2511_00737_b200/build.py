@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libephdc.so")
 OBJ = os.path.join(os.path.dirname(HERE), "build", "obj")
-SOURCES = ["api.cu", "kernels.cu", "kernels_f64.cu", "ntt_c5.cu", "encode_tc.cu", "noise.cu", "host_math.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "kernels_f64.cu", "ntt_c5.cu", "ntt32_c5.cu", "encode_tc.cu", "noise.cu", "host_math.cpp"]
 HEADERS = ["internal.h", "modarith.cuh", "ntt_dev.cuh", "modf64.cuh", "ntt_f64.cuh", "tmem.cuh", "tmem_x.cuh", "tma_host.h", "async_copy.cuh",
            "rng.cuh", "host_math.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -960,7 +960,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
                                    ephdc_ntt_plan **out) {
     if (!q || !out) return EPHDC_ENULL;
     *out = nullptr;
-    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16 || (flags & ~(EPHDC_NTT_FORCE_INT | EPHDC_NTT_ALT_TEAMS)))
+    if (L < 1 || L > EPHDC_MAX_PRIMES || log2N < 10 || log2N > 16 || (flags & ~(EPHDC_NTT_FORCE_INT | EPHDC_NTT_ALT_TEAMS | EPHDC_NTT_U32_GENERIC)))
         return EPHDC_EPARAM;
     for (uint32_t j = 0; j < L; ++j)
         if (q[j] >= (1ull << 61) || !is_ntt_prime(q[j], log2N)) return EPHDC_EPARAM;
@@ -992,6 +992,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
     if (flags & EPHDC_NTT_FORCE_INT) p->fwd_f64 = p->inv_f64 = false;
     p->c5_alt_teams = (flags & EPHDC_NTT_ALT_TEAMS) != 0;
     p->int_per_poly = p->c5_alt_teams;
+    p->u32_generic = (flags & EPHDC_NTT_U32_GENERIC) != 0;
     // the c5 kernels (ntt_c5.cu) use the FP64 forward table at every N >= 2^12 whose
     // primes are all < 2^50; their own bounds are decided in plan_ntt_c5
     const bool c5_candidate = !(flags & EPHDC_NTT_FORCE_INT) && log2N >= 12 &&
@@ -1119,7 +1120,9 @@ ephdc_status ephdc_ntt_fwd32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     if (!p->tw32) return EPHDC_EPARAM;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    EPHDC_CUDA_TRY(launch_ntt_batch32(p, d_polys, batch, false, (cudaStream_t)stream));
+    const cudaError_t e = launch_ntt32_c5(p, d_polys, batch, false, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch32(p, d_polys, batch, false, (cudaStream_t)stream));
+    else EPHDC_CUDA_TRY(e);
     return EPHDC_OK;
 }
 
@@ -1127,7 +1130,9 @@ ephdc_status ephdc_ntt_inv32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     if (!p->tw32) return EPHDC_EPARAM;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    EPHDC_CUDA_TRY(launch_ntt_batch32(p, d_polys, batch, true, (cudaStream_t)stream));
+    const cudaError_t e = launch_ntt32_c5(p, d_polys, batch, true, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch32(p, d_polys, batch, true, (cudaStream_t)stream));
+    else EPHDC_CUDA_TRY(e);
     return EPHDC_OK;
 }
 
@@ -1145,6 +1150,9 @@ ephdc_status ephdc_ntt_plan_query(const ephdc_ntt_plan *p, ephdc_ntt_plan_info *
     info->fwd_kernel = p->c5_fwd ? EPHDC_NTT_KERNEL_C5_F64 : p->fwd_f64 ? EPHDC_NTT_KERNEL_F64 : EPHDC_NTT_KERNEL_INT;
     info->inv_kernel = p->c5_inv ? EPHDC_NTT_KERNEL_C5_F64 : p->inv_f64 ? EPHDC_NTT_KERNEL_F64 : EPHDC_NTT_KERNEL_INT;
     info->u32_words = p->tw32 != nullptr;
+    info->u32_kernel = !p->tw32 ? EPHDC_NTT_KERNEL_INT
+                       : (!p->u32_generic && p->log2N >= 12 && p->log2N <= 14) ? EPHDC_NTT_KERNEL_C5_U32
+                                                                               : EPHDC_NTT_KERNEL_INT;
     return EPHDC_OK;
 }
 

@@ -142,6 +142,7 @@ struct ephdc_ntt_plan {
     bool c5_fwd = false, c5_inv = false, c5_red = false;
     bool c5_alt_teams = false;   // EPHDC_NTT_ALT_TEAMS (A/B only)
     bool int_per_poly = false;   // EPHDC_NTT_ALT_TEAMS also selects the per-polynomial integer kernel (A/B)
+    bool u32_generic = false;    // EPHDC_NTT_U32_GENERIC: the general u32 kernels instead of ntt32_c5.cu (A/B)
     // inverse: DIT table [L][N] (W[h + jj] = omega^-(N/2h) jj, entry 0 = (q, 1/q)), fused
     // level-12 scaling [L][NC/2][2] (sigma_r, sigma_r W[NC/2 + r]), sigma_r = N^-1 psi^-r;
     // c_loc = psi^-(NC/2); block constants c_k = psi^-(NC k) [L][8]
@@ -229,6 +230,9 @@ struct C5Args {
 cudaError_t plan_ntt_c5(ephdc_ntt_plan *p);
 void ephdc_ntt_plan_c5_free(ephdc_ntt_plan *p);
 cudaError_t launch_ntt_c5(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t batch, bool inverse, cudaStream_t st);
+// c5 u32 kernels (ntt32_c5.cu) at N = 2^12 .. 2^14; cudaErrorNotSupported elsewhere
+cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, bool inverse,
+                            cudaStream_t st);
 bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan);
 void f64_grid(const ephdc_ctx *c, uint32_t nb, uint32_t *bg, uint32_t *chunks, uint32_t *G);
 int ntt_mac_occupancy(uint32_t log2N, uint32_t S);

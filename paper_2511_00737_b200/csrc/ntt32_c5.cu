@@ -1,0 +1,370 @@
+// ntt32_c5.cu -- the c5 standalone negacyclic NTT on u32 words (every prime < 2^30;
+// BASELINE.json configs[4], SURVEY 8(d) "30-bit primes in u32"), integer pipe.
+//
+// The textbook loops of oracle/oracle_core.c (forward Cooley-Tukey over psi_rev, inverse
+// Gentleman-Sande over psiinv_rev then N^-1; P:1458-1459 counts one forward NTT per
+// plaintext), with u32 Shoup products and Harvey's lazy ranges (modarith.cuh: forward
+// values in [0, 4q), inverse in [0, 2q); 4q < 2^32 because q < 2^30).
+//
+// In place on [batch][L][N] canonical u32, N = NC = 2^12, 2^13, 2^14 (one CTA per
+// polynomial; 2^15 / 2^16 keep the general kernels).  Per CTA, NT = NC/32 threads with
+// 32 elements each, persistent over a contiguous range of prime-major items:
+//   * polynomials arrive by TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B: word e of a
+//     1024-byte-aligned buffer sits at sw(e) = e ^ (((e >> 5) & 7) << 2)) into a ring
+//     of three buffers -- the load of item i+3 is issued once item i has been stored;
+//     results leave by a TMA store of the same buffer (cp.async.bulk.tensor ...
+//     bulk_group);
+//   * forward levels in three register passes, all conflict-free in the swizzled
+//     layout and all with compile-time offsets from per-group bases:
+//       A  levels 0 .. LG-10:  groups {g + 512k} (lanes consecutive),
+//       B  levels LG-9 .. LG-6: groups {512 blk + off + 32k}, off = lane (a 32-word row
+//          holds one k, so the XOR term depends on k & 7 only: 8 bases),
+//       C  levels LG-5 .. LG-1: one 32-word row per thread, read and written as eight
+//          16-byte chunks (chunk m of row g sits at m ^ (g & 7): a quarter warp touches 8
+//          distinct chunks);
+//     the inverse runs C (half-sizes 1..16), B (32..256), A (512..NC/2) with the
+//     scaling by N^-1 fused into the last level: (X + Y) N^-1 and (X - Y) (w N^-1);
+//   * twiddles: the levels of A and B are warp-uniform (broadcast reads of the first
+//     NC/32 table entries in shared memory); the 31 (w, w') pairs of a thread's row in
+//     pass C live in TENSOR MEMORY (64 columns per thread), loaded once per prime.
+// DESIGN.md 5.2 "c5 u32 kernels".
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "async_copy.cuh"
+#include "internal.h"
+#include "modarith.cuh"
+#include "tma_host.h"
+#include "tmem_x.cuh"
+
+namespace ephdc {
+namespace c5u32 {
+
+constexpr int kE = 32;      // elements per thread
+constexpr int kNBuf = 3;    // rotating polynomial buffers
+
+template <int LG> __host__ __device__ constexpr int nthreads() { return (1 << LG) / kE; }
+template <int LG> __host__ __device__ constexpr int ctas_per_sm() { return LG == 12 ? 4 : LG == 13 ? 2 : 1; }
+// 64 TMEM columns per thread (31 pairs); warps w and w + 4 share a lane quarter
+template <int LG> __host__ __device__ constexpr uint32_t tmem_cols() { return 64u * (uint32_t)((nthreads<LG>() / 32 + 3) / 4); }
+template <int LG> __host__ __device__ constexpr int box_rows() { return (1 << LG) / 32 > 256 ? 256 : (1 << LG) / 32; }
+template <int LG> __host__ __device__ constexpr size_t smem_bytes() {
+    return 1024 + sizeof(u32) * kNBuf * ((size_t)1 << LG) + sizeof(TwPair<u32>) * (((size_t)1 << LG) >> 5);
+}
+
+struct Args {
+    u32 L, batch, items;
+    const TwPair<u32> *tw;   // [L][N] psi_rev (forward) or psiinv_rev (inverse), Shoup pairs
+    const u32 *ninv;         // [L][2] (N^-1, Shoup)
+    u32 q[kMaxL];
+};
+
+EPHDC_D int sw(int e) { return e ^ (((e >> 5) & 7) << 2); }
+
+EPHDC_D void tma_load(void *dst, const CUtensorMap *map, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            ephdc_async::smem_u32(dst)),
+        "l"(map), "r"(0), "r"(y), "r"(ephdc_async::smem_u32(bar))
+        : "memory");
+}
+EPHDC_D void tma_store(const CUtensorMap *map, int y, const void *src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(0), "r"(y),
+                 "r"(ephdc_async::smem_u32(src))
+                 : "memory");
+}
+EPHDC_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+EPHDC_D void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+EPHDC_D void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct Prime {
+    u32 q, two_q;
+    TwPair<u32> ninv, wn;   // inverse: N^-1 and w N^-1 (w = psiinv_rev[1]) for the last level
+};
+
+// Register sub-stages with compile-time trip counts (template recursion: ptxas keeps
+// x[] in registers).  CT sub-stage sub pairs (k, k + R/2^(sub+1)) of sub-block v, twiddle
+// tw(sub, v); GS sub-stage sub pairs (k, k + 2^sub) of block v = k >> (sub+1).
+template <int R_LOG, int SUB, int END, class Tw>
+EPHDC_D void ct_subs(u32 (&x)[1 << R_LOG], const Tw &tw, u32 q, u32 two_q) {
+    if constexpr (SUB < END) {
+        constexpr int R = 1 << R_LOG, h = R >> (SUB + 1);
+#pragma unroll
+        for (int v = 0; v < (1 << SUB); ++v) {
+            const TwPair<u32> t = tw(SUB, v);
+#pragma unroll
+            for (int kk = 0; kk < h; ++kk) ct_bfly<u32>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], t, q, two_q);
+        }
+        ct_subs<R_LOG, SUB + 1, END>(x, tw, q, two_q);
+    }
+}
+template <int R_LOG, int SUB, int END, class Tw>
+EPHDC_D void gs_subs(u32 (&x)[1 << R_LOG], const Tw &tw, u32 q, u32 two_q) {
+    if constexpr (SUB < END) {
+        constexpr int R = 1 << R_LOG, hs = 1 << SUB;
+#pragma unroll
+        for (int v = 0; v < R / (2 * hs); ++v) {
+            const TwPair<u32> t = tw(SUB, v);
+#pragma unroll
+            for (int kk = 0; kk < hs; ++kk) gs_bfly<u32>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], t, q, two_q);
+        }
+        gs_subs<R_LOG, SUB + 1, END>(x, tw, q, two_q);
+    }
+}
+
+// ---- pass A: R = 2^(LG-9) elements {g + 512k} per group, 32/R groups per thread ----
+template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwPair<u32> *tws, const Prime &pr, int tid) {
+    constexpr int NC = 1 << LG, NT = NC / kE, RA = LG - 9, R = 1 << RA, GA = kE / R;
+#pragma unroll
+    for (int u = 0; u < GA; ++u) {
+        u32 *P = B + sw(tid + u * NT);   // sw(g + 512k) = sw(g) + 512k (g < 512)
+        u32 x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[k] = P[512 * k];
+        if constexpr (!INV) {   // levels 0 .. RA-1: psi_rev[2^sub + v]
+            ct_subs<RA, 0, RA>(x, [&](int sub, int v) { return tws[(1 << sub) + v]; }, pr.q, pr.two_q);
+        } else {   // half-sizes 2^(9+sub): psiinv_rev[NC/2^(10+sub) + v]; the last one fused with N^-1
+            gs_subs<RA, 0, RA - 1>(x, [&](int sub, int v) { return tws[(NC >> (10 + sub)) + v]; }, pr.q, pr.two_q);
+            constexpr int hs = R / 2;
+#pragma unroll
+            for (int kk = 0; kk < hs; ++kk) {
+                const u32 X = x[kk], Y = x[kk + hs];
+                x[kk] = csub(mul_shoup_lazy<u32>(X + Y, pr.ninv.w, pr.ninv.wp, pr.q), pr.q);
+                x[kk + hs] = csub(mul_shoup_lazy<u32>(X - Y + pr.two_q, pr.wn.w, pr.wn.wp, pr.q), pr.q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) P[512 * k] = x[k];
+    }
+}
+
+// ---- pass B: 16 elements {512 blk + off + 32k} per group, two groups per thread ----
+template <int LG, bool INV> EPHDC_D void pass_b(u32 *B, const TwPair<u32> *tws, const Prime &pr, int tid) {
+    constexpr int NC = 1 << LG, NT = NC / kE;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int g = tid + u * NT, blk = g >> 5, off = g & 31;
+        u32 *P = B + blk * 512;
+        int o[8];   // row k holds word off at off ^ ((k & 7) << 2)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) o[c] = off ^ (c << 2);
+        u32 x[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = P[o[k & 7] + 32 * k];
+        if constexpr (!INV)   // level LG-9+sub, block blk 2^sub + v
+            ct_subs<4, 0, 4>(x, [&](int sub, int v) { return tws[((NC >> 9) << sub) + (blk << sub) + v]; }, pr.q, pr.two_q);
+        else                  // half-size 2^(5+sub): psiinv_rev[NC/2^(6+sub) + blk 2^(3-sub) + v]
+            gs_subs<4, 0, 4>(x, [&](int sub, int v) { return tws[(NC >> (6 + sub)) + (blk << (3 - sub)) + v]; }, pr.q,
+                             pr.two_q);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) P[o[k & 7] + 32 * k] = x[k];
+    }
+}
+
+EPHDC_D TwPair<u32> tpair(const uint32_t (&r0)[32], const uint32_t (&r1)[32], int p) {
+    return p < 16 ? TwPair<u32>{r0[2 * p], r0[2 * p + 1]} : TwPair<u32>{r1[2 * p - 32], r1[2 * p - 31]};
+}
+
+// ---- pass C: the thread's 32-word row, 16-byte chunks; twiddle pairs from TMEM ----
+template <int LG, bool INV> EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid) {
+    uint32_t r0[32], r1[32];
+    ephdc_tmem::ldx<32>(tbase, r0);
+    ephdc_tmem::ldx<32>(tbase + 32u, r1);
+    u32 *P = B + 32 * tid;
+    const int g7 = tid & 7;
+    u32 x[32];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(P + 4 * (m ^ g7));
+        x[4 * m] = v.x;
+        x[4 * m + 1] = v.y;
+        x[4 * m + 2] = v.z;
+        x[4 * m + 3] = v.w;
+    }
+    ephdc_tmem::waitx<32>(r0);
+    ephdc_tmem::waitx<32>(r1);
+    if constexpr (!INV) {   // level LG-5+sub, pair (2^sub - 1) + v
+        ct_subs<5, 0, 5>(x, [&](int sub, int v) { return tpair(r0, r1, (1 << sub) - 1 + v); }, pr.q, pr.two_q);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) x[k] = reduce4<u32>(x[k], pr.q, pr.two_q);
+    } else {   // half-size 2^s, pair 32 - 2^(5-s) + v
+        gs_subs<5, 0, 5>(x, [&](int s, int v) { return tpair(r0, r1, 32 - (32 >> s) + v); }, pr.q, pr.two_q);
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+        *reinterpret_cast<uint4 *>(P + 4 * (m ^ g7)) = make_uint4(x[4 * m], x[4 * m + 1], x[4 * m + 2], x[4 * m + 3]);
+}
+
+template <int LG, bool INV>
+__global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
+    k_ntt32_c5(const __grid_constant__ CUtensorMap map, const __grid_constant__ Args a) {
+    constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5;
+    constexpr int kBox = box_rows<LG>(), kBoxes = NC / 32 / kBox;
+    static_assert(LG >= 12 && LG <= 14, "one CTA per polynomial, 2^12 .. 2^14");
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t mbar[kNBuf];
+    __shared__ uint32_t tmem_slot;
+    u32 *bufs = reinterpret_cast<u32 *>(smem_raw + ((1024u - (ephdc_async::smem_u32(smem_raw) & 1023u)) & 1023u));
+    TwPair<u32> *tws = reinterpret_cast<TwPair<u32> *>(bufs + kNBuf * NC);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0)
+        for (int b = 0; b < kNBuf; ++b) ephdc_async::mbar_init(&mbar[b], 1);
+    if (warp == 0) ephdc_tmem::alloc(&tmem_slot, tmem_cols<LG>());
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    const uint32_t tbase = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 64u;
+
+    const u32 w0 = (u32)((u64)a.items * blockIdx.x / gridDim.x), w1 = (u32)((u64)a.items * (blockIdx.x + 1) / gridDim.x);
+    const u32 n = w1 - w0;
+    auto row_of = [&](u32 w) -> int {   // first 128-byte row of item w (prime-major items)
+        const u32 j = w / a.batch, b = w - j * a.batch;
+        return (int)((((size_t)b * a.L + j) << LG) >> 5);
+    };
+    auto issue = [&](u32 i) {   // one thread
+        uint64_t *bar = &mbar[i % kNBuf];
+        u32 *dst = bufs + (i % kNBuf) * NC;
+        ephdc_async::mbar_arrive_expect_tx(bar, (u32)(NC * 4));
+        const int y = row_of(w0 + i);
+#pragma unroll
+        for (int k = 0; k < kBoxes; ++k) tma_load(dst + k * kBox * 32, &map, y + k * kBox, bar);
+    };
+    if (tid == 0)
+        for (u32 i = 0; i < (u32)kNBuf && i < n; ++i) issue(i);
+
+    u32 jcur = 0xffffffffu;
+    Prime pr{0, 0, {0, 0}, {0, 0}};
+    for (u32 i = 0; i < n; ++i) {
+        const u32 w = w0 + i, j = w / a.batch;
+        if (j != jcur) {   // the previous item's last barrier freed the twiddles
+            const TwPair<u32> *gt = a.tw + ((size_t)j << LG);
+            for (int p = tid; p < NTW; p += NT) tws[p] = gt[p];
+            uint32_t r[16];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int p = 8 * h + c;
+                    TwPair<u32> t{0, 0};
+                    if (p < 31) {
+                        int idx;
+                        if constexpr (!INV) {   // level LG-5+sub, block tid 2^sub + v: psi_rev[NC/32 2^sub + ...]
+                            const int sub = 31 - __clz(p + 1), v = p + 1 - (1 << sub);
+                            idx = ((NC >> 5) << sub) + (tid << sub) + v;
+                        } else {                // half-size 2^s: psiinv_rev[NC/2^(s+1) + tid 2^(4-s) + v]
+                            const int s = p < 16 ? 0 : p < 24 ? 1 : p < 28 ? 2 : p < 30 ? 3 : 4;
+                            const int v = p - (32 - (32 >> s));
+                            idx = (NC >> (s + 1)) + (tid << (4 - s)) + v;
+                        }
+                        t = gt[idx];
+                    }
+                    r[2 * c] = t.w;
+                    r[2 * c + 1] = t.wp;
+                }
+                ephdc_tmem::stx<16>(tbase + 16u * h, r);
+            }
+            ephdc_tmem::wait_st();
+            pr.q = a.q[j];
+            pr.two_q = 2 * pr.q;
+            if constexpr (INV) {
+                pr.ninv = TwPair<u32>{a.ninv[2 * j], a.ninv[2 * j + 1]};
+                const u32 wv = (u32)(((u64)gt[1].w * pr.ninv.w) % pr.q);
+                pr.wn = TwPair<u32>{wv, (u32)(((u64)wv << 32) / pr.q)};
+            }
+            jcur = j;
+            __syncthreads();
+        }
+        u32 *B = bufs + (i % kNBuf) * NC;
+        ephdc_async::mbar_wait(&mbar[i % kNBuf], (i / kNBuf) & 1);
+        if constexpr (!INV) {
+            pass_a<LG, false>(B, tws, pr, tid);
+            __syncthreads();
+            pass_b<LG, false>(B, tws, pr, tid);
+            __syncthreads();
+            pass_c<LG, false>(B, tbase, pr, tid);
+        } else {
+            pass_c<LG, true>(B, tbase, pr, tid);
+            __syncthreads();
+            pass_b<LG, true>(B, tws, pr, tid);
+            __syncthreads();
+            pass_a<LG, true>(B, tws, pr, tid);
+        }
+        ephdc_async::fence_proxy_async();   // this thread's writes -> the TMA store
+        __syncthreads();
+        if (tid == 0) {
+            const int y = row_of(w);
+#pragma unroll
+            for (int k = 0; k < kBoxes; ++k) tma_store(&map, y + k * kBox, B + k * kBox * 32);
+            bulk_commit();
+            if (i + kNBuf < n) {
+                bulk_wait_read0();   // the store has read the buffer
+                issue(i + kNBuf);
+            }
+        }
+    }
+    if (tid == 0) bulk_wait0();
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    if (warp == 0) ephdc_tmem::dealloc(tmem_slot, tmem_cols<LG>());
+}
+
+inline cudaError_t counted(cudaError_t e) {
+    if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+    return e;
+}
+
+// [n_words / 32] rows of 128 bytes, box box_rows x 128 bytes, 128-byte swizzle
+bool make_map32(CUtensorMap *m, const void *base, uint64_t n_words, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn || (n_words & 31) || (n_words >> 5) > 0x7fffffffull) return false;
+    const cuuint64_t dims[2] = {32, n_words >> 5};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {32u, box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int LG, bool INV>
+cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cudaStream_t st) {
+    auto kern = k_ntt32_c5<LG, INV>;
+    constexpr size_t smem = smem_bytes<LG>();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    CUtensorMap map;
+    if (!make_map32(&map, polys, (uint64_t)batch * p->L * p->N, (uint32_t)box_rows<LG>())) return cudaErrorNotSupported;
+    Args a{};
+    a.L = p->L;
+    a.batch = batch;
+    a.items = p->L * batch;
+    a.tw = INV ? p->itw32 : p->tw32;
+    a.ninv = p->ninv32;
+    for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
+    const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * ctas_per_sm<LG>(), a.items));
+    kern<<<units, nthreads<LG>(), smem, st>>>(map, a);
+    return counted(cudaGetLastError());
+}
+
+}  // namespace c5u32
+
+// The c5 u32 kernels where they apply (N = 2^12 .. 2^14, unless the plan asks for the
+// general kernels); cudaErrorNotSupported otherwise (the caller runs the general ones).
+cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, bool inverse,
+                            cudaStream_t st) {
+    if (p->u32_generic || !p->tw32) return cudaErrorNotSupported;
+    if (batch == 0) return cudaSuccess;
+    if ((uint64_t)batch * p->L > 0xffffffffull || ((uintptr_t)d_polys & 15)) return cudaErrorNotSupported;
+    using namespace c5u32;
+    switch (p->log2N) {
+        case 12: return inverse ? launch<12, true>(p, d_polys, batch, st) : launch<12, false>(p, d_polys, batch, st);
+        case 13: return inverse ? launch<13, true>(p, d_polys, batch, st) : launch<13, false>(p, d_polys, batch, st);
+        case 14: return inverse ? launch<14, true>(p, d_polys, batch, st) : launch<14, false>(p, d_polys, batch, st);
+    }
+    return cudaErrorNotSupported;
+}
+
+}  // namespace ephdc

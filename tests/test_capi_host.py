@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(_capi.lib, s), s
     assert set(syms) == set(_capi.EXPORTED)
-    assert _capi.lib.ephdc_abi_version() == 3
+    assert _capi.lib.ephdc_abi_version() == 4
 
 
 def test_library_is_sm100a_only():

@@ -170,3 +170,46 @@ def test_u32_words_need_small_primes():
     assert not plan.u32_words
     with pytest.raises(eph.EphdcError):
         eph.ntt_fwd32(plan, torch.zeros((1, 1, 4096), dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("log2N", [12, 13, 14])
+@pytest.mark.parametrize("L,batch", [(1, 1), (3, 2), (5, 7), (16, 3), (2, 149), (3, 301), (1, 1000)])
+def test_ntt_c5_u32_kernels(log2N, L, batch):
+    """The persistent TMA-fed u32 kernels (ntt32_c5.cu: swizzled in-place passes, TMEM row
+    twiddles, TMA store) = the oracle's NTT on sampled polynomials of every prime, = the
+    general u32 kernels (EPHDC_NTT_U32_GENERIC) on the whole batch, and inverse(forward(x))
+    = x -- at batches that give CTAs one item, items of two primes, and many items."""
+    N = 1 << log2N
+    q = nt.prime_chain([30] * L, log2N)
+    x = inp.gen_residues(q, batch, N, seed=4000 + 10 * log2N + L + batch)
+    pc, pg = eph.NttPlan(q, log2N), eph.NttPlan(q, log2N, u32_generic=True)
+    assert pc.u32_kernel == "c5_u32" and pg.u32_kernel == "int_u32"
+    dc = torch.from_numpy(x.astype(np.int32)).cuda()
+    dg = dc.clone()
+    eph.ntt_fwd32(pc, dc)
+    eph.ntt_fwd32(pg, dg)
+    assert torch.equal(dc, dg)
+    got = dc.cpu().numpy().astype(np.uint32).astype(np.uint64)
+    rng = np.random.default_rng(batch)
+    for b in sorted({0, batch - 1, int(rng.integers(0, batch))}):
+        for j in range(L):
+            psi = nt.min_primitive_2n_root(q[j], N)
+            assert np.array_equal(got[b, j], core.ntt_fwd(x[b, j][None, :], log2N, q[j], psi)[0]), (b, j)
+    eph.ntt_inv32(pc, dc)
+    eph.ntt_inv32(pg, dg)
+    assert torch.equal(dc, dg)
+    assert np.array_equal(dc.cpu().numpy().astype(np.uint32).astype(np.uint64), x)
+
+
+def test_ntt_c5_u32_inverse_vs_oracle():
+    """Inverse alone (not only as the forward's inverse) against the oracle's INTT."""
+    log2N, L, N = 13, 3, 1 << 13
+    q = nt.prime_chain([30] * L, log2N)
+    x = inp.gen_residues(q, 5, N, seed=4242)
+    p = eph.NttPlan(q, log2N)
+    d = torch.from_numpy(x.astype(np.int32)).cuda()
+    eph.ntt_inv32(p, d)
+    got = d.cpu().numpy().astype(np.uint32).astype(np.uint64)
+    for j in range(L):
+        psi = nt.min_primitive_2n_root(q[j], N)
+        assert np.array_equal(got[:, j], core.ntt_inv(x[:, j], log2N, q[j], psi)), j

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--only", default="", help="lg:L:bits:wordbytes[,...]")
     ap.add_argument("--max-batch-only", action="store_true", help="time only the largest batch of each point")
     ap.add_argument("--alt-teams", action="store_true", help="A/B: the other warp layout of the c5 kernels at N = 2^13")
+    ap.add_argument("--u32-generic", action="store_true", help="A/B: the general u32 kernels instead of ntt32_c5.cu")
     a = ap.parse_args()
     import torch
     import ephdc_inputs as inp
@@ -64,7 +65,7 @@ def main():
             continue
         N = 1 << lg
         q = eph.find_ntt_primes(lg, [bits] * L)
-        plan = eph.NttPlan(q, lg, alt_teams=a.alt_teams)
+        plan = eph.NttPlan(q, lg, alt_teams=a.alt_teams, u32_generic=a.u32_generic)
         if wb == 4 and not plan.u32_words:
             continue
         fwd, inv, mac = (eph.ntt_fwd, eph.ntt_inv, eph.mac) if wb == 8 else (eph.ntt_fwd32, eph.ntt_inv32, eph.mac32)
@@ -84,8 +85,8 @@ def main():
                 res[name] = {"ms": round(ms, 5), "GB_s": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4),
                              "butterflies_G_s": round(batch * L * (N // 2) * lg / (ms / 1e3) / 1e9, 1)}
             res["clocks"] = clk.stop()
-            res["kernels"] = {"fwd": plan.fwd_kernel if wb == 8 else "int_u32",
-                              "inv": plan.inv_kernel if wb == 8 else "int_u32"}
+            res["kernels"] = {"fwd": plan.fwd_kernel if wb == 8 else plan.u32_kernel,
+                              "inv": plan.inv_kernel if wb == 8 else plan.u32_kernel}
             print(json.dumps({"workload": "c5", "log2N": lg, "alt_teams": a.alt_teams, "L": L, "bits": bits, "word_bits": 8 * wb,
                               "batch": batch, "bytes_per_launch": 2 * batch * per_poly, "hbm_peak_gbs": hbm,
                               **res}), flush=True)

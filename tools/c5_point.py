@@ -24,14 +24,17 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="polynomials (0: a 2 GiB working set)")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--alt-teams", action="store_true")
+    ap.add_argument("--u32", action="store_true", help="u32 words (30-bit primes): ephdc_ntt_fwd32 / inv32")
+    ap.add_argument("--u32-generic", action="store_true", help="with --u32: the general u32 kernels")
     a = ap.parse_args()
     import torch
     import paper_2511_00737_b200 as eph
 
     N = 1 << a.lg
     q = eph.find_ntt_primes(a.lg, [a.bits] * a.L)
-    plan = eph.NttPlan(q, a.lg, alt_teams=a.alt_teams)
-    per_poly = a.L * N * 8
+    plan = eph.NttPlan(q, a.lg, alt_teams=a.alt_teams, u32_generic=a.u32_generic)
+    wb = 4 if a.u32 else 8
+    per_poly = a.L * N * wb
     dev = torch.device("cuda", 0)
     qt = torch.tensor(q, dtype=torch.int64, device=dev)
     if a.op == "mac":
@@ -44,7 +47,11 @@ def main():
     else:
         batch = a.batch or max(1, (2 << 30) // per_poly)
         x = torch.remainder(torch.randint(0, 1 << 62, (batch, a.L, N), dtype=torch.int64, device=dev), qt.view(1, -1, 1))
-        f = eph.ntt_fwd if a.op == "fwd" else eph.ntt_inv
+        if a.u32:
+            x = x.to(torch.int32)
+            f = eph.ntt_fwd32 if a.op == "fwd" else eph.ntt_inv32
+        else:
+            f = eph.ntt_fwd if a.op == "fwd" else eph.ntt_inv
         fn = lambda: f(plan, x)  # noqa: E731
         nbytes = 2 * batch * per_poly
     fn()
