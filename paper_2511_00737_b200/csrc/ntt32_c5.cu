@@ -59,6 +59,7 @@ struct Args {
     const TwPair<u32> *tw;   // [L][N] psi_rev (forward) or psiinv_rev (inverse), Shoup pairs
     const u32 *ninv;         // [L][2] (N^-1, Shoup)
     u32 q[kMaxL];
+    u32 zero;                // 0: a runtime addend that keeps the butterfly sums 3-input IADD3s
 };
 
 EPHDC_D int sw(int e) { return e ^ (((e >> 5) & 7) << 2); }
@@ -80,42 +81,66 @@ EPHDC_D void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;"
 EPHDC_D void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 struct Prime {
-    u32 q, two_q;
+    u32 q, two_q, z;
     TwPair<u32> ninv, wn;   // inverse: N^-1 and w N^-1 (w = psiinv_rev[1]) for the last level
 };
 
 // Register sub-stages with compile-time trip counts (template recursion: ptxas keeps
 // x[] in registers).  CT sub-stage sub pairs (k, k + R/2^(sub+1)) of sub-block v, twiddle
 // tw(sub, v); GS sub-stage sub pairs (k, k + 2^sub) of block v = k >> (sub+1).
-template <int R_LOG, int SUB, int END, class Tw>
-EPHDC_D void ct_subs(u32 (&x)[1 << R_LOG], const Tw &tw, u32 q, u32 two_q) {
+template <int R_LOG, int SUB, int END, class Tw, class Bf>
+EPHDC_D void ct_subs(u32 (&x)[1 << R_LOG], const Tw &tw, const Bf &bf) {
     if constexpr (SUB < END) {
         constexpr int R = 1 << R_LOG, h = R >> (SUB + 1);
 #pragma unroll
         for (int v = 0; v < (1 << SUB); ++v) {
-            const TwPair<u32> t = tw(SUB, v);
+            const auto t = tw(SUB, v);
 #pragma unroll
-            for (int kk = 0; kk < h; ++kk) ct_bfly<u32>(x[v * 2 * h + kk], x[v * 2 * h + kk + h], t, q, two_q);
+            for (int kk = 0; kk < h; ++kk) bf(x[v * 2 * h + kk], x[v * 2 * h + kk + h], t);
         }
-        ct_subs<R_LOG, SUB + 1, END>(x, tw, q, two_q);
+        ct_subs<R_LOG, SUB + 1, END>(x, tw, bf);
     }
 }
-template <int R_LOG, int SUB, int END, class Tw>
-EPHDC_D void gs_subs(u32 (&x)[1 << R_LOG], const Tw &tw, u32 q, u32 two_q) {
+template <int R_LOG, int SUB, int END, class Tw, class Bf>
+EPHDC_D void gs_subs(u32 (&x)[1 << R_LOG], const Tw &tw, const Bf &bf) {
     if constexpr (SUB < END) {
         constexpr int R = 1 << R_LOG, hs = 1 << SUB;
 #pragma unroll
         for (int v = 0; v < R / (2 * hs); ++v) {
-            const TwPair<u32> t = tw(SUB, v);
+            const auto t = tw(SUB, v);
 #pragma unroll
-            for (int kk = 0; kk < hs; ++kk) gs_bfly<u32>(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], t, q, two_q);
+            for (int kk = 0; kk < hs; ++kk) bf(x[v * 2 * hs + kk], x[v * 2 * hs + kk + hs], t);
         }
-        gs_subs<R_LOG, SUB + 1, END>(x, tw, q, two_q);
+        gs_subs<R_LOG, SUB + 1, END>(x, tw, bf);
     }
 }
 
+// Shared-memory twiddle of passes A and B (a Shoup pair).
+typedef TwPair<u32> TwH;
+
+// butterfly functors: Shoup pairs (pass C, TMEM) and the shared TwH entries (A, B)
+// Harvey butterflies (modarith.cuh ct_bfly / gs_bfly) with the two-input sums written
+// as three-input sums with a runtime zero: ptxas then issues IADD3 on the ALU pipe
+// instead of IMAD.IADD on the IMAD pipe, which the Shoup products already load.
+EPHDC_D auto ct_shoup(const Prime &pr) {
+    return [&pr](u32 &X, u32 &Y, const TwPair<u32> &t) {
+        const u32 x = csub(X, pr.two_q), r = mul_shoup_lazy<u32>(Y, t.w, t.wp, pr.q);
+        X = x + r + pr.z;
+        Y = x - r + pr.two_q;
+    };
+}
+EPHDC_D auto gs_shoup(const Prime &pr) {
+    return [&pr](u32 &X, u32 &Y, const TwPair<u32> &t) {
+        const u32 x = X, y = Y;
+        X = csub(x + y + pr.z, pr.two_q);
+        Y = mul_shoup_lazy<u32>(x - y + pr.two_q, t.w, t.wp, pr.q);
+    };
+}
+EPHDC_D auto ct_ab(const Prime &pr) { return ct_shoup(pr); }
+EPHDC_D auto gs_ab(const Prime &pr) { return gs_shoup(pr); }
+
 // ---- pass A: R = 2^(LG-9) elements {g + 512k} per group, 32/R groups per thread ----
-template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwPair<u32> *tws, const Prime &pr, int tid) {
+template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwH *tws, const Prime &pr, int tid) {
     constexpr int NC = 1 << LG, NT = NC / kE, RA = LG - 9, R = 1 << RA, GA = kE / R;
 #pragma unroll
     for (int u = 0; u < GA; ++u) {
@@ -124,9 +149,9 @@ template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwPair<u32> *tws, 
 #pragma unroll
         for (int k = 0; k < R; ++k) x[k] = P[512 * k];
         if constexpr (!INV) {   // levels 0 .. RA-1: psi_rev[2^sub + v]
-            ct_subs<RA, 0, RA>(x, [&](int sub, int v) { return tws[(1 << sub) + v]; }, pr.q, pr.two_q);
+            ct_subs<RA, 0, RA>(x, [&](int sub, int v) { return tws[(1 << sub) + v]; }, ct_ab(pr));
         } else {   // half-sizes 2^(9+sub): psiinv_rev[NC/2^(10+sub) + v]; the last one fused with N^-1
-            gs_subs<RA, 0, RA - 1>(x, [&](int sub, int v) { return tws[(NC >> (10 + sub)) + v]; }, pr.q, pr.two_q);
+            gs_subs<RA, 0, RA - 1>(x, [&](int sub, int v) { return tws[(NC >> (10 + sub)) + v]; }, gs_ab(pr));
             constexpr int hs = R / 2;
 #pragma unroll
             for (int kk = 0; kk < hs; ++kk) {
@@ -141,7 +166,7 @@ template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwPair<u32> *tws, 
 }
 
 // ---- pass B: 16 elements {512 blk + off + 32k} per group, two groups per thread ----
-template <int LG, bool INV> EPHDC_D void pass_b(u32 *B, const TwPair<u32> *tws, const Prime &pr, int tid) {
+template <int LG, bool INV> EPHDC_D void pass_b(u32 *B, const TwH *tws, const Prime &pr, int tid) {
     constexpr int NC = 1 << LG, NT = NC / kE;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -154,10 +179,10 @@ template <int LG, bool INV> EPHDC_D void pass_b(u32 *B, const TwPair<u32> *tws, 
 #pragma unroll
         for (int k = 0; k < 16; ++k) x[k] = P[o[k & 7] + 32 * k];
         if constexpr (!INV)   // level LG-9+sub, block blk 2^sub + v
-            ct_subs<4, 0, 4>(x, [&](int sub, int v) { return tws[((NC >> 9) << sub) + (blk << sub) + v]; }, pr.q, pr.two_q);
+            ct_subs<4, 0, 4>(x, [&](int sub, int v) { return tws[((NC >> 9) << sub) + (blk << sub) + v]; }, ct_ab(pr));
         else                  // half-size 2^(5+sub): psiinv_rev[NC/2^(6+sub) + blk 2^(3-sub) + v]
-            gs_subs<4, 0, 4>(x, [&](int sub, int v) { return tws[(NC >> (6 + sub)) + (blk << (3 - sub)) + v]; }, pr.q,
-                             pr.two_q);
+            gs_subs<4, 0, 4>(x, [&](int sub, int v) { return tws[(NC >> (6 + sub)) + (blk << (3 - sub)) + v]; },
+                             gs_ab(pr));
 #pragma unroll
         for (int k = 0; k < 16; ++k) P[o[k & 7] + 32 * k] = x[k];
     }
@@ -186,11 +211,11 @@ template <int LG, bool INV> EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Pr
     ephdc_tmem::waitx<32>(r0);
     ephdc_tmem::waitx<32>(r1);
     if constexpr (!INV) {   // level LG-5+sub, pair (2^sub - 1) + v
-        ct_subs<5, 0, 5>(x, [&](int sub, int v) { return tpair(r0, r1, (1 << sub) - 1 + v); }, pr.q, pr.two_q);
+        ct_subs<5, 0, 5>(x, [&](int sub, int v) { return tpair(r0, r1, (1 << sub) - 1 + v); }, ct_shoup(pr));
 #pragma unroll
         for (int k = 0; k < 32; ++k) x[k] = reduce4<u32>(x[k], pr.q, pr.two_q);
     } else {   // half-size 2^s, pair 32 - 2^(5-s) + v
-        gs_subs<5, 0, 5>(x, [&](int s, int v) { return tpair(r0, r1, 32 - (32 >> s) + v); }, pr.q, pr.two_q);
+        gs_subs<5, 0, 5>(x, [&](int s, int v) { return tpair(r0, r1, 32 - (32 >> s) + v); }, gs_shoup(pr));
     }
 #pragma unroll
     for (int m = 0; m < 8; ++m)
@@ -207,7 +232,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
     __shared__ __align__(8) uint64_t mbar[kNBuf];
     __shared__ uint32_t tmem_slot;
     u32 *bufs = reinterpret_cast<u32 *>(smem_raw + ((1024u - (ephdc_async::smem_u32(smem_raw) & 1023u)) & 1023u));
-    TwPair<u32> *tws = reinterpret_cast<TwPair<u32> *>(bufs + kNBuf * NC);
+    TwH *tws = reinterpret_cast<TwH *>(bufs + kNBuf * NC);
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0)
         for (int b = 0; b < kNBuf; ++b) ephdc_async::mbar_init(&mbar[b], 1);
@@ -235,7 +260,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
         for (u32 i = 0; i < (u32)kNBuf && i < n; ++i) issue(i);
 
     u32 jcur = 0xffffffffu;
-    Prime pr{0, 0, {0, 0}, {0, 0}};
+    Prime pr{0, 0, a.zero, {0, 0}, {0, 0}};
     for (u32 i = 0; i < n; ++i) {
         const u32 w = w0 + i, j = w / a.batch;
         if (j != jcur) {   // the previous item's last barrier freed the twiddles
@@ -344,6 +369,7 @@ cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cud
     a.tw = INV ? p->itw32 : p->tw32;
     a.ninv = p->ninv32;
     for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
+    a.zero = 0;
     const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * ctas_per_sm<LG>(), a.items));
     kern<<<units, nthreads<LG>(), smem, st>>>(map, a);
     return counted(cudaGetLastError());
