@@ -3,7 +3,8 @@
 The default plan (f64_grid + the WL / prefetch choice in mac_f64_launch) is checked
 against the oracle by test_gpu_fullsize / test_gpu_parity; every other variant the
 workspace plan overrides (ephdc_plan) select must produce exactly the same scores ciphertexts:
-the two-group kernel (the NC = 2^13 default) against the one-team kernel, the
+the two-group kernel (the NC = 2^13 default) against the one-team kernel, the round-1
+slot pack + INTT_t kernel against the ntt32_c5.cu one, the
 synchronisation variants WL = 0/1/2, 32 elements per thread, the explicit L2
 prefetch on/off, and other grid plans (batches per group, dims per chunk -- i.e. other
 orders of the 64-bit atomic folds, which integer addition makes order independent).
@@ -40,6 +41,7 @@ VARIANTS = [
     {"flags": 32, "G": 37},
     {"flags": 64},           # the two-group kernel at N = 2^14 (c4; one team by default)
     {"flags": 64, "bg": 1, "G": 37},
+    {"flags": 128},          # the round-1 slot pack + INTT_t kernel (default: ntt32_c5.cu passes)
 ]
 
 
