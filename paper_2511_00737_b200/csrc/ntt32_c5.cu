@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "async_copy.cuh"
 #include "internal.h"
@@ -47,11 +48,16 @@ constexpr int kNBuf = 3;    // rotating polynomial buffers
 
 template <int LG> __host__ __device__ constexpr int nthreads() { return (1 << LG) / kE; }
 template <int LG> __host__ __device__ constexpr int ctas_per_sm() { return LG == 12 ? 4 : LG == 13 ? 2 : 1; }
+// OCC (A/B): two buffers per CTA, so that 6 / 3 CTAs fit an SM at 2^12 / 2^13 (<= 80 registers)
+template <int LG, bool OCC> __host__ __device__ constexpr int nbuf() { return OCC && LG <= 13 ? 2 : kNBuf; }
+template <int LG, bool OCC> __host__ __device__ constexpr int cps() {
+    return OCC && LG <= 13 ? (LG == 12 ? 6 : 3) : ctas_per_sm<LG>();
+}
 // 64 TMEM columns per thread (31 pairs); warps w and w + 4 share a lane quarter
 template <int LG> __host__ __device__ constexpr uint32_t tmem_cols() { return 64u * (uint32_t)((nthreads<LG>() / 32 + 3) / 4); }
 template <int LG> __host__ __device__ constexpr int box_rows() { return (1 << LG) / 32 > 256 ? 256 : (1 << LG) / 32; }
-template <int LG> __host__ __device__ constexpr size_t smem_bytes() {
-    return 1024 + sizeof(u32) * kNBuf * ((size_t)1 << LG) + sizeof(TwPair<u32>) * (((size_t)1 << LG) >> 5);
+template <int LG, bool OCC> __host__ __device__ constexpr size_t smem_bytes() {
+    return 1024 + sizeof(u32) * nbuf<LG, OCC>() * ((size_t)1 << LG) + sizeof(TwPair<u32>) * (((size_t)1 << LG) >> 5);
 }
 
 struct Args {
@@ -140,7 +146,13 @@ EPHDC_D auto ct_ab(const Prime &pr) { return ct_shoup(pr); }
 EPHDC_D auto gs_ab(const Prime &pr) { return gs_shoup(pr); }
 
 // ---- pass A: R = 2^(LG-9) elements {g + 512k} per group, 32/R groups per thread ----
-template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwH *tws, const Prime &pr, int tid) {
+struct ToSmem {
+    EPHDC_D void operator()(int, u32) const {}
+};
+// (Out: the inverse's output element e goes to out(e, value) instead of B)
+template <int LG, bool INV, class Out = ToSmem>
+EPHDC_D void pass_a(u32 *B, const TwH *tws, const Prime &pr, int tid, const Out &out = Out()) {
+    constexpr bool kOut = !std::is_same<Out, ToSmem>::value;
     constexpr int NC = 1 << LG, NT = NC / kE, RA = LG - 9, R = 1 << RA, GA = kE / R;
 #pragma unroll
     for (int u = 0; u < GA; ++u) {
@@ -160,8 +172,13 @@ template <int LG, bool INV> EPHDC_D void pass_a(u32 *B, const TwH *tws, const Pr
                 x[kk + hs] = csub(mul_shoup_lazy<u32>(X - Y + pr.two_q, pr.wn.w, pr.wn.wp, pr.q), pr.q);
             }
         }
+        if constexpr (kOut) {
 #pragma unroll
-        for (int k = 0; k < R; ++k) P[512 * k] = x[k];
+            for (int k = 0; k < R; ++k) out(tid + u * NT + 512 * k, x[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < R; ++k) P[512 * k] = x[k];
+        }
     }
 }
 
@@ -193,7 +210,14 @@ EPHDC_D TwPair<u32> tpair(const uint32_t (&r0)[32], const uint32_t (&r1)[32], in
 }
 
 // ---- pass C: the thread's 32-word row, 16-byte chunks; twiddle pairs from TMEM ----
-template <int LG, bool INV> EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid) {
+struct FromSmem {
+    EPHDC_D u32 operator()(int) const { return 0u; }
+};
+// (Load: the inverse's input element i of the row comes from load(i) instead of B --
+// the slot pack of the query path)
+template <int LG, bool INV, class Load = FromSmem>
+EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid, const Load &load = Load()) {
+    constexpr bool kLoad = !std::is_same<Load, FromSmem>::value;
     uint32_t r0[32], r1[32];
     ephdc_tmem::ldx<32>(tbase, r0);
     ephdc_tmem::ldx<32>(tbase + 32u, r1);
@@ -202,11 +226,16 @@ template <int LG, bool INV> EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Pr
     u32 x[32];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(P + 4 * (m ^ g7));
-        x[4 * m] = v.x;
-        x[4 * m + 1] = v.y;
-        x[4 * m + 2] = v.z;
-        x[4 * m + 3] = v.w;
+        if constexpr (kLoad) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) x[4 * m + c] = load(32 * tid + 4 * m + c);
+        } else {
+            const uint4 v = *reinterpret_cast<const uint4 *>(P + 4 * (m ^ g7));
+            x[4 * m] = v.x;
+            x[4 * m + 1] = v.y;
+            x[4 * m + 2] = v.z;
+            x[4 * m + 3] = v.w;
+        }
     }
     ephdc_tmem::waitx<32>(r0);
     ephdc_tmem::waitx<32>(r1);
@@ -222,20 +251,20 @@ template <int LG, bool INV> EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Pr
         *reinterpret_cast<uint4 *>(P + 4 * (m ^ g7)) = make_uint4(x[4 * m], x[4 * m + 1], x[4 * m + 2], x[4 * m + 3]);
 }
 
-template <int LG, bool INV>
-__global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
+template <int LG, bool INV, bool OCC>
+__global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     k_ntt32_c5(const __grid_constant__ CUtensorMap map, const __grid_constant__ Args a) {
-    constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5;
+    constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5, kNB = nbuf<LG, OCC>();
     constexpr int kBox = box_rows<LG>(), kBoxes = NC / 32 / kBox;
     static_assert(LG >= 12 && LG <= 14, "one CTA per polynomial, 2^12 .. 2^14");
     extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t mbar[kNBuf];
+    __shared__ __align__(8) uint64_t mbar[kNB];
     __shared__ uint32_t tmem_slot;
     u32 *bufs = reinterpret_cast<u32 *>(smem_raw + ((1024u - (ephdc_async::smem_u32(smem_raw) & 1023u)) & 1023u));
-    TwH *tws = reinterpret_cast<TwH *>(bufs + kNBuf * NC);
+    TwH *tws = reinterpret_cast<TwH *>(bufs + kNB * NC);
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0)
-        for (int b = 0; b < kNBuf; ++b) ephdc_async::mbar_init(&mbar[b], 1);
+        for (int b = 0; b < kNB; ++b) ephdc_async::mbar_init(&mbar[b], 1);
     if (warp == 0) ephdc_tmem::alloc(&tmem_slot, tmem_cols<LG>());
     ephdc_tmem::fence_before_sync();
     __syncthreads();
@@ -249,15 +278,15 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
         return (int)((((size_t)b * a.L + j) << LG) >> 5);
     };
     auto issue = [&](u32 i) {   // one thread
-        uint64_t *bar = &mbar[i % kNBuf];
-        u32 *dst = bufs + (i % kNBuf) * NC;
+        uint64_t *bar = &mbar[i % kNB];
+        u32 *dst = bufs + (i % kNB) * NC;
         ephdc_async::mbar_arrive_expect_tx(bar, (u32)(NC * 4));
         const int y = row_of(w0 + i);
 #pragma unroll
         for (int k = 0; k < kBoxes; ++k) tma_load(dst + k * kBox * 32, &map, y + k * kBox, bar);
     };
     if (tid == 0)
-        for (u32 i = 0; i < (u32)kNBuf && i < n; ++i) issue(i);
+        for (u32 i = 0; i < (u32)kNB && i < n; ++i) issue(i);
 
     u32 jcur = 0xffffffffu;
     Prime pr{0, 0, a.zero, {0, 0}, {0, 0}};
@@ -301,8 +330,8 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
             jcur = j;
             __syncthreads();
         }
-        u32 *B = bufs + (i % kNBuf) * NC;
-        ephdc_async::mbar_wait(&mbar[i % kNBuf], (i / kNBuf) & 1);
+        u32 *B = bufs + (i % kNB) * NC;
+        ephdc_async::mbar_wait(&mbar[i % kNB], (i / kNB) & 1);
         if constexpr (!INV) {
             pass_a<LG, false>(B, tws, pr, tid);
             __syncthreads();
@@ -323,13 +352,95 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
 #pragma unroll
             for (int k = 0; k < kBoxes; ++k) tma_store(&map, y + k * kBox, B + k * kBox * 32);
             bulk_commit();
-            if (i + kNBuf < n) {
+            if (i + kNB < n) {
                 bulk_wait_read0();   // the store has read the buffer
-                issue(i + kNBuf);
+                issue(i + kNB);
             }
         }
     }
     if (tid == 0) bulk_wait0();
+    ephdc_tmem::fence_before_sync();
+    __syncthreads();
+    ephdc_tmem::fence_after_sync();
+    if (warp == 0) ephdc_tmem::dealloc(tmem_slot, tmem_cols<LG>());
+}
+
+// =====================================================================================
+// The query path's slot pack + INTT mod t ("EncPt"; K2 of DESIGN.md) on the same
+// passes: row (b, d) of M [nbat][D][N] = centered lift of INTT_t(slots), slot i holding
+// h[d][b B + i/k] for i < k n_b (reading #1), 0 beyond.  Pass C reads the
+// slots of its row straight from H (int8 [D][nq]) instead of shared memory, pass A
+// writes the centered int32 results straight to M (lanes consecutive: coalesced).  Two
+// row buffers alternate, so a row costs two CTA barriers.  Persistent over rows.
+// =====================================================================================
+struct PackArgs32 {
+    u32 t, ninv, ninv_p, k, B, D, nq, b0, nbat, kmagic, zero;
+    const TwPair<u32> *itw;   // [N] psiinv_rev mod t, Shoup pairs
+};
+
+template <int LG>
+__global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
+    k_pack_intt32(const int8_t *__restrict__ H, PackArgs32 a, u32 *__restrict__ M) {
+    constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint32_t tmem_slot;
+    u32 *bufs = reinterpret_cast<u32 *>(smem_raw + ((1024u - (ephdc_async::smem_u32(smem_raw) & 1023u)) & 1023u));
+    TwH *tws = reinterpret_cast<TwH *>(bufs + 2 * NC);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) ephdc_tmem::alloc(&tmem_slot, tmem_cols<LG>());
+    for (int p = tid; p < NTW; p += NT) tws[p] = a.itw[p];
+    {   // this thread's row twiddles (inverse order, as in k_ntt32_c5)
+        uint32_t r[16];
+        ephdc_tmem::fence_before_sync();
+        __syncthreads();
+        ephdc_tmem::fence_after_sync();
+        const uint32_t tb = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 64u;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int p = 8 * h + c;
+                TwPair<u32> t{0, 0};
+                if (p < 31) {
+                    const int s = p < 16 ? 0 : p < 24 ? 1 : p < 28 ? 2 : p < 30 ? 3 : 4;
+                    t = a.itw[(NC >> (s + 1)) + (tid << (4 - s)) + (p - (32 - (32 >> s)))];
+                }
+                r[2 * c] = t.w;
+                r[2 * c + 1] = t.wp;
+            }
+            ephdc_tmem::stx<16>(tb + 16u * h, r);
+        }
+        ephdc_tmem::wait_st();
+    }
+    const uint32_t tbase = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 64u;
+    Prime pr{a.t, 2 * a.t, a.zero, {a.ninv, a.ninv_p}, {0, 0}};
+    {
+        const u32 wv = (u32)(((u64)a.itw[1].w * a.ninv) % a.t);
+        pr.wn = TwPair<u32>{wv, (u32)(((u64)wv << 32) / a.t)};
+    }
+    const u32 half_t = (a.t - 1) / 2;
+    __syncthreads();
+    const u32 rows = a.nbat * a.D;
+    u32 par = 0;
+    for (u32 row = blockIdx.x; row < rows; row += gridDim.x, par ^= 1u) {
+        const u32 bb = row / a.D, d = row - bb * a.D, b = a.b0 + bb;
+        const u32 lim = a.k * min(a.B, a.nq - b * a.B);
+        const int8_t *src = H + (size_t)d * a.nq + (size_t)b * a.B;
+        u32 *B = bufs + par * NC;
+        auto load = [&](int i) -> u32 {   // slot i -> h[d][b B + i/k] mod t
+            if ((u32)i >= lim) return 0u;
+            const int v = __ldg(src + (a.k == 1u ? (u32)i : __umulhi((u32)i, a.kmagic)));
+            return v < 0 ? (u32)((int)a.t + v) : (u32)v;
+        };
+        pass_c<LG, true>(B, tbase, pr, tid, load);
+        __syncthreads();
+        pass_b<LG, true>(B, tws, pr, tid);
+        __syncthreads();
+        u32 *o = M + (size_t)row * NC;
+        pass_a<LG, true>(B, tws, pr, tid, [&](int e, u32 y) {
+            o[e] = y <= half_t ? y : (u32)((int)y - (int)a.t);   // centered lift (reading #3)
+        });
+    }
     ephdc_tmem::fence_before_sync();
     __syncthreads();
     ephdc_tmem::fence_after_sync();
@@ -356,8 +467,9 @@ bool make_map32(CUtensorMap *m, const void *base, uint64_t n_words, uint32_t box
 
 template <int LG, bool INV>
 cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cudaStream_t st) {
-    auto kern = k_ntt32_c5<LG, INV>;
-    constexpr size_t smem = smem_bytes<LG>();
+    // (EPHDC_NTT_ALT_TEAMS: the OCC variant, A/B)
+    auto kern = p->c5_alt_teams ? k_ntt32_c5<LG, INV, true> : k_ntt32_c5<LG, INV, false>;
+    const size_t smem = p->c5_alt_teams ? smem_bytes<LG, true>() : smem_bytes<LG, false>();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap map;
@@ -370,7 +482,7 @@ cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cud
     a.ninv = p->ninv32;
     for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
     a.zero = 0;
-    const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * ctas_per_sm<LG>(), a.items));
+    const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * (p->c5_alt_teams ? cps<LG, true>() : cps<LG, false>()), a.items));
     kern<<<units, nthreads<LG>(), smem, st>>>(map, a);
     return counted(cudaGetLastError());
 }
@@ -389,6 +501,41 @@ cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t
         case 12: return inverse ? launch<12, true>(p, d_polys, batch, st) : launch<12, false>(p, d_polys, batch, st);
         case 13: return inverse ? launch<13, true>(p, d_polys, batch, st) : launch<13, false>(p, d_polys, batch, st);
         case 14: return inverse ? launch<14, true>(p, d_polys, batch, st) : launch<14, false>(p, d_polys, batch, st);
+    }
+    return cudaErrorNotSupported;
+}
+
+// Slot pack + INTT_t of the query path at N = 2^12 .. 2^14 (cudaErrorNotSupported below).
+cudaError_t launch_pack_intt_q32(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b0, uint32_t nbat,
+                                 uint32_t *d_M, cudaStream_t st) {
+    using namespace c5u32;
+    PackArgs32 a{};
+    a.t = (u32)c->t;
+    a.ninv = c->ninv_t;
+    a.ninv_p = c->ninv_t_p;
+    a.k = c->p.k;
+    a.B = c->B;
+    a.D = c->p.D_live;
+    a.nq = nq;
+    a.b0 = b0;
+    a.nbat = nbat;
+    a.kmagic = c->p.k > 1 ? (u32)((1ull << 32) / c->p.k + 1) : 0u;   // k = 1: identity
+    a.zero = 0;
+    a.itw = c->dev.itw_t;
+    const uint64_t rows = (uint64_t)nbat * a.D;
+    if (rows == 0) return cudaSuccess;
+    auto go = [&](auto kern, int lg) -> cudaError_t {
+        const u32 grid = (u32)std::min<uint64_t>(rows, 148ull * (lg == 12 ? 4 : lg == 13 ? 2 : 1));
+        const size_t smem = 1024 + sizeof(u32) * 2 * ((size_t)1 << lg) + sizeof(TwPair<u32>) * (((size_t)1 << lg) >> 5);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, (1u << lg) / kE, smem, st>>>(d_H, a, d_M);
+        return counted(cudaGetLastError());
+    };
+    switch (c->p.log2N) {
+        case 12: return go(k_pack_intt32<12>, 12);
+        case 13: return go(k_pack_intt32<13>, 13);
+        case 14: return go(k_pack_intt32<14>, 14);
     }
     return cudaErrorNotSupported;
 }
