@@ -467,9 +467,12 @@ bool make_map32(CUtensorMap *m, const void *base, uint64_t n_words, uint32_t box
 
 template <int LG, bool INV>
 cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cudaStream_t st) {
-    // (EPHDC_NTT_ALT_TEAMS: the OCC variant, A/B)
-    auto kern = p->c5_alt_teams ? k_ntt32_c5<LG, INV, true> : k_ntt32_c5<LG, INV, false>;
-    const size_t smem = p->c5_alt_teams ? smem_bytes<LG, true>() : smem_bytes<LG, false>();
+    // inverse: the OCC form (two buffers, 3 / 6 CTAs per SM at 2^13 / 2^12: 0.546 vs
+    // 0.531 of HBM at 2^13); forward: three buffers (0.525 vs 0.526; r47).
+    // EPHDC_NTT_ALT_TEAMS swaps the forms (A/B).
+    const bool occ = INV != p->c5_alt_teams;
+    auto kern = occ ? k_ntt32_c5<LG, INV, true> : k_ntt32_c5<LG, INV, false>;
+    const size_t smem = occ ? smem_bytes<LG, true>() : smem_bytes<LG, false>();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap map;
@@ -482,7 +485,7 @@ cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cud
     a.ninv = p->ninv32;
     for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
     a.zero = 0;
-    const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * (p->c5_alt_teams ? cps<LG, true>() : cps<LG, false>()), a.items));
+    const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * (occ ? cps<LG, true>() : cps<LG, false>()), a.items));
     kern<<<units, nthreads<LG>(), smem, st>>>(map, a);
     return counted(cudaGetLastError());
 }
