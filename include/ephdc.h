@@ -417,7 +417,7 @@ ephdc_status ephdc_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
 /* The same three operations on 32-bit words (30-bit primes in u32): every
  * array is uint32 with the layouts above; the plan's primes must all be < 2^30
  * (EPARAM otherwise).  Integer-pipe u32 Shoup butterflies; MAC products accumulate
- * exactly in 64 bits.  Async. */
+ * exactly in 64 bits (ephdc_mac32: d_ct and d_pt 16-byte aligned, else ECUDA).  Async. */
 ephdc_status ephdc_ntt_fwd32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, void *stream);
 ephdc_status ephdc_ntt_inv32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, void *stream);
 ephdc_status ephdc_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,

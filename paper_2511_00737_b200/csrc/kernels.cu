@@ -715,40 +715,55 @@ __global__ void __launch_bounds__(256) k_ntt_global(W *__restrict__ polys, u32 n
 }
 
 // Standalone MAC on u32 words (primes < 2^30): products < 2^60 accumulate exactly in u64
-// and are reduced every 15 terms (15 * 2^60 < 2^64); the per-split partial sums (< q)
-// are folded with 64-bit atomics into out64 [L][2][N], reduced by k_mac32_out.
+// and are reduced every 15 terms (15 * 2^60 + q < 2^64) by a Barrett step with
+// m = floor((2^64 - 1) / q); the per-split partial sums (< q) are folded with 64-bit
+// atomics into out64 [L][2][N], reduced by k_mac32_out.  A thread owns 4 consecutive
+// coefficients (16-byte streaming loads) and keeps 5 terms' loads in flight.
+EPHDC_D u64 barrett64(u64 x, u64 q, u64 m) {
+    u64 r = x - mulhi(x, m) * q;   // floor(x m / 2^64) >= floor(x / q) - 2: r < 3q
+    r = r >= q ? r - q : r;
+    return r >= q ? r - q : r;
+}
 __global__ void __launch_bounds__(256) k_mac32(const u32 *__restrict__ ct, const u32 *__restrict__ pt, u32 D, u32 L,
                                                u32 N, u32 dsplit, PrimeSet ps, u64 *__restrict__ out) {
-    const u32 pairs = (L * N) >> 1;
+    const u32 quads = (L * N) >> 2;
     const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= pairs) return;
-    const u32 lin = 2 * g, j = lin / N, i = lin % N;
-    const u64 q = ps.q[j];
+    if (g >= quads) return;
+    const u32 lin = 4 * g, j = lin / N, i = lin % N;
+    const u64 q = ps.q[j], m = ~0ull / q;
     const u32 per = (D + dsplit - 1) / dsplit;
     const u32 d0 = blockIdx.y * per, d1 = min(D, d0 + per);
-    u64 a00 = 0, a01 = 0, a10 = 0, a11 = 0;
-    u32 n = 0;
-    for (u32 d = d0; d < d1; ++d) {
-        const uint2 p = __ldcs(reinterpret_cast<const uint2 *>(pt + ((size_t)d * L + j) * N + i));
-        const uint2 c0 = __ldcs(reinterpret_cast<const uint2 *>(ct + (((size_t)d * L + j) * 2) * N + i));
-        const uint2 c1 = __ldcs(reinterpret_cast<const uint2 *>(ct + (((size_t)d * L + j) * 2 + 1) * N + i));
-        a00 += (u64)c0.x * p.x;
-        a01 += (u64)c0.y * p.y;
-        a10 += (u64)c1.x * p.x;
-        a11 += (u64)c1.y * p.y;
-        if (++n == 15) {
-            n = 0;
-            a00 %= q;
-            a01 %= q;
-            a10 %= q;
-            a11 %= q;
+    u64 a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+    const size_t sp = (size_t)L * N, sc = 2 * sp;   // strides of one term
+    const u32 *pp = pt + (size_t)j * N + i, *cp = ct + (size_t)j * 2 * N + i;
+    for (u32 d = d0; d < d1; d += 15) {
+        const u32 e = min(d1, d + 15);
+#pragma unroll 5
+        for (u32 dd = d; dd < e; ++dd) {
+            const uint4 p = __ldcs(reinterpret_cast<const uint4 *>(pp + dd * sp));
+            const uint4 c0 = __ldcs(reinterpret_cast<const uint4 *>(cp + dd * sc));
+            const uint4 c1 = __ldcs(reinterpret_cast<const uint4 *>(cp + dd * sc + N));
+            a0[0] += (u64)c0.x * p.x;
+            a0[1] += (u64)c0.y * p.y;
+            a0[2] += (u64)c0.z * p.z;
+            a0[3] += (u64)c0.w * p.w;
+            a1[0] += (u64)c1.x * p.x;
+            a1[1] += (u64)c1.y * p.y;
+            a1[2] += (u64)c1.z * p.z;
+            a1[3] += (u64)c1.w * p.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            a0[k] = barrett64(a0[k], q, m);
+            a1[k] = barrett64(a1[k], q, m);
         }
     }
     unsigned long long *o = reinterpret_cast<unsigned long long *>(out + (size_t)j * 2 * N + i);
-    atomicAdd(o, a00 % q);
-    atomicAdd(o + 1, a01 % q);
-    atomicAdd(o + N, a10 % q);
-    atomicAdd(o + N + 1, a11 % q);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        atomicAdd(o + k, a0[k]);
+        atomicAdd(o + N + k, a1[k]);
+    }
 }
 
 __global__ void k_mac32_out(const u64 *__restrict__ acc, u32 L, u32 N, PrimeSet ps, u32 *__restrict__ out) {
@@ -1186,12 +1201,13 @@ cudaError_t launch_ntt_batch32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint3
 cudaError_t launch_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,
                          uint32_t *d_out, cudaStream_t st) {
     const u32 L = p->L, N = p->N;
+    if (((uintptr_t)d_ct | (uintptr_t)d_pt) & 15) return cudaErrorMisalignedAddress;   // 16-byte loads
     u64 *acc = nullptr;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&acc), sizeof(u64) * 2 * L * N, st);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(acc, 0, sizeof(u64) * 2 * L * N, st);
-    const u32 pairs = (L * N) / 2;
-    const u32 bx = (pairs + 255) / 256;
+    const u32 quads = (L * N) / 4;
+    const u32 bx = (quads + 255) / 256;
     // <= 2^16 partial sums < q < 2^30 per coefficient: the 64-bit fold cannot wrap
     u32 dsplit = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
     dsplit = std::max<u32>(1, std::min(std::min(dsplit, D), 1u << 16));
