@@ -772,32 +772,58 @@ __global__ void k_mac32_out(const u64 *__restrict__ acc, u32 L, u32 N, PrimeSet 
     out[i] = (u32)(acc[i] % ps.q[i / (2 * N)]);
 }
 
-// Standalone MAC: each thread owns 2 consecutive coefficients of one prime, loops over a d-range.
+// Standalone MAC for primes >= 2^50 (u64 words): the exact 128-bit products are summed in
+// 128-bit accumulators (32 terms of < 2^122 stay below 2^127) and folded to [0, q) every
+// 32 terms with two Montgomery products: hi 2^64 + lo = mont(hi, 2^128 mod q) +
+// mont(lo, 2^64 mod q) (mod q) -- one 64x64 -> 128 product per term instead of a
+// Montgomery product (4 wide multiplies).  Each thread owns 2 consecutive coefficients of
+// one prime and keeps 4 terms' loads in flight; outputs are true residues (k_mod_q).
+struct U128 {
+    u64 lo, hi;
+};
+EPHDC_D void mac128(U128 &acc, u64 a, u64 b) {
+    const u64 lo = a * b, hi = mulhi(a, b);
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(acc.lo), "+l"(acc.hi) : "l"(lo), "l"(hi));
+}
+EPHDC_D u64 fold128(const U128 &x, u64 q, u64 qinv, u64 r2, u64 r1) {
+    const u64 t = mont_mul(x.hi, r2, q, qinv) + mont_mul(x.lo, r1, q, qinv);   // < 2q
+    return t >= q ? t - q : t;
+}
 __global__ void __launch_bounds__(256) k_mac(const u64 *__restrict__ ct, const u64 *__restrict__ pt, u32 D, u32 L,
                                              u32 N, u32 dsplit, PrimeSet ps, u64 *__restrict__ out) {
     const u32 pairs = (L * N) >> 1;
     const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= pairs) return;
     const u32 lin = 2 * g, j = lin / N, i = lin % N;
-    const u64 q = ps.q[j], qinv = ps.qinv[j];
+    const u64 q = ps.q[j], qinv = ps.qinv[j], r2 = ps.r2[j];
+    const u64 r1 = mont_mul(r2, 1, q, qinv);   // 2^64 mod q
     const u32 per = (D + dsplit - 1) / dsplit;
     const u32 d0 = blockIdx.y * per, d1 = min(D, d0 + per);
-    u64 a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+    U128 a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
+    const size_t sp = (size_t)L * N, sc = 2 * sp;
+    const u64 *pp = pt + (size_t)j * N + i, *cp = ct + (size_t)j * 2 * N + i;
+    for (u32 d = d0; d < d1; d += 32) {
+        const u32 e = min(d1, d + 32);
 #pragma unroll 4
-    for (u32 d = d0; d < d1; ++d) {
-        const ulonglong2 p = __ldcs(reinterpret_cast<const ulonglong2 *>(pt + ((size_t)d * L + j) * N + i));
-        const ulonglong2 c0 = __ldcs(reinterpret_cast<const ulonglong2 *>(ct + (((size_t)d * L + j) * 2) * N + i));
-        const ulonglong2 c1 = __ldcs(reinterpret_cast<const ulonglong2 *>(ct + (((size_t)d * L + j) * 2 + 1) * N + i));
-        a00 = csub(a00 + mont_mul(c0.x, p.x, q, qinv), q);
-        a01 = csub(a01 + mont_mul(c0.y, p.y, q, qinv), q);
-        a10 = csub(a10 + mont_mul(c1.x, p.x, q, qinv), q);
-        a11 = csub(a11 + mont_mul(c1.y, p.y, q, qinv), q);
+        for (u32 dd = d; dd < e; ++dd) {
+            const ulonglong2 p = __ldcs(reinterpret_cast<const ulonglong2 *>(pp + dd * sp));
+            const ulonglong2 c0 = __ldcs(reinterpret_cast<const ulonglong2 *>(cp + dd * sc));
+            const ulonglong2 c1 = __ldcs(reinterpret_cast<const ulonglong2 *>(cp + dd * sc + N));
+            mac128(a00, c0.x, p.x);
+            mac128(a01, c0.y, p.y);
+            mac128(a10, c1.x, p.x);
+            mac128(a11, c1.y, p.y);
+        }
+        a00 = U128{fold128(a00, q, qinv, r2, r1), 0};
+        a01 = U128{fold128(a01, q, qinv, r2, r1), 0};
+        a10 = U128{fold128(a10, q, qinv, r2, r1), 0};
+        a11 = U128{fold128(a11, q, qinv, r2, r1), 0};
     }
     unsigned long long *o = reinterpret_cast<unsigned long long *>(out + (size_t)j * 2 * N + i);
-    atomicAdd(o, a00);
-    atomicAdd(o + 1, a01);
-    atomicAdd(o + N, a10);
-    atomicAdd(o + N + 1, a11);
+    atomicAdd(o, a00.lo);
+    atomicAdd(o + 1, a01.lo);
+    atomicAdd(o + N, a10.lo);
+    atomicAdd(o + N + 1, a11.lo);
 }
 
 // The same MAC on the FP64 pipe for primes < 2^50 (modf64.cuh: exact products in
@@ -1249,9 +1275,8 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
     k_mac<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, d_out);
     e = counted(cudaGetLastError());
     if (e != cudaSuccess) return e;
-    // finalize: output layout [L][2][N]
-    // reuse k_finalize with the [j][c][i] layout: prime index = i / (2N)
-    k_finalize<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
+    // output layout [L][2][N]: prime index = i / (2N); the folded sums are true residues
+    k_mod_q<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
     return counted(cudaGetLastError());
 }
 
