@@ -213,3 +213,31 @@ def test_ntt_c5_u32_inverse_vs_oracle():
     for j in range(L):
         psi = nt.min_primitive_2n_root(q[j], N)
         assert np.array_equal(got[:, j], core.ntt_inv(x[:, j], log2N, q[j], psi)), j
+
+
+def test_ntt_c5_u32_stress_repeated_launches():
+    """The TMA/mbarrier ring of ntt32_c5.cu under repetition: 120 forward + inverse
+    launches at seeded random sizes (N = 2^12..2^14, 1..16 primes, 1..2500 polynomials),
+    each checked to round-trip exactly, every tenth against the general u32 kernels."""
+    rng = np.random.default_rng(2024)
+    plans = {}
+    for it in range(120):
+        log2N = int(rng.integers(12, 15))
+        L = int(rng.integers(1, 17))
+        batch = int(rng.integers(1, 2501 if log2N < 14 else 801))
+        key = (log2N, L)
+        if key not in plans:
+            q = nt.prime_chain([30] * L, log2N)
+            plans[key] = (q, eph.NttPlan(q, log2N), eph.NttPlan(q, log2N, u32_generic=True))
+        q, pc, pg = plans[key]
+        qt = torch.tensor(q, dtype=torch.int64, device="cuda").view(1, L, 1)
+        x = torch.remainder(torch.randint(0, 1 << 31, (batch, L, 1 << log2N), device="cuda", dtype=torch.int64), qt)
+        x = x.to(torch.int32)
+        d = x.clone()
+        eph.ntt_fwd32(pc, d)
+        if it % 10 == 0:
+            g = x.clone()
+            eph.ntt_fwd32(pg, g)
+            assert torch.equal(d, g), (it, log2N, L, batch)
+        eph.ntt_inv32(pc, d)
+        assert torch.equal(d, x), (it, log2N, L, batch)
