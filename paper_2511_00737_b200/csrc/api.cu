@@ -1088,6 +1088,7 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
             return EPHDC_ECUDA;
         }
     }
+    p->u32_for_u64 = p->tw32 && !p->u32_generic && !(flags & EPHDC_NTT_FORCE_INT) && log2N >= 12 && log2N <= 14;
     if (c5_candidate && plan_ntt_c5(p.get()) != cudaSuccess) {
         ephdc_ntt_plan_free(p.release());
         return EPHDC_ECUDA;
@@ -1099,7 +1100,8 @@ ephdc_status ephdc_ntt_plan_create(const uint64_t *q, uint32_t L, uint32_t log2N
 ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    cudaError_t e = launch_ntt_c5(p, d_polys, batch, false, (cudaStream_t)stream);
+    cudaError_t e = launch_ntt32_c5_u64(p, d_polys, batch, false, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) e = launch_ntt_c5(p, d_polys, batch, false, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) e = launch_ntt_batch_f64(p, d_polys, batch, false, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, false, (cudaStream_t)stream));
     else EPHDC_CUDA_TRY(e);
@@ -1109,7 +1111,8 @@ ephdc_status ephdc_ntt_fwd(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t 
 ephdc_status ephdc_ntt_inv(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, void *stream) {
     if (!p || (!d_polys && batch)) return EPHDC_ENULL;
     EPHDC_CUDA_TRY(cudaSetDevice(p->device));
-    cudaError_t e = launch_ntt_c5(p, d_polys, batch, true, (cudaStream_t)stream);
+    cudaError_t e = launch_ntt32_c5_u64(p, d_polys, batch, true, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) e = launch_ntt_c5(p, d_polys, batch, true, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) e = launch_ntt_batch_f64(p, d_polys, batch, true, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) EPHDC_CUDA_TRY(launch_ntt_batch(p, d_polys, batch, true, (cudaStream_t)stream));
     else EPHDC_CUDA_TRY(e);
@@ -1147,8 +1150,14 @@ ephdc_status ephdc_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const ui
 
 ephdc_status ephdc_ntt_plan_query(const ephdc_ntt_plan *p, ephdc_ntt_plan_info *info) {
     if (!p || !info) return EPHDC_ENULL;
-    info->fwd_kernel = p->c5_fwd ? EPHDC_NTT_KERNEL_C5_F64 : p->fwd_f64 ? EPHDC_NTT_KERNEL_F64 : EPHDC_NTT_KERNEL_INT;
-    info->inv_kernel = p->c5_inv ? EPHDC_NTT_KERNEL_C5_F64 : p->inv_f64 ? EPHDC_NTT_KERNEL_F64 : EPHDC_NTT_KERNEL_INT;
+    info->fwd_kernel = p->u32_for_u64 ? EPHDC_NTT_KERNEL_C5_U32
+                       : p->c5_fwd    ? EPHDC_NTT_KERNEL_C5_F64
+                       : p->fwd_f64   ? EPHDC_NTT_KERNEL_F64
+                                      : EPHDC_NTT_KERNEL_INT;
+    info->inv_kernel = p->u32_for_u64 ? EPHDC_NTT_KERNEL_C5_U32
+                       : p->c5_inv    ? EPHDC_NTT_KERNEL_C5_F64
+                       : p->inv_f64   ? EPHDC_NTT_KERNEL_F64
+                                      : EPHDC_NTT_KERNEL_INT;
     info->u32_words = p->tw32 != nullptr;
     info->u32_kernel = !p->tw32 ? EPHDC_NTT_KERNEL_INT
                        : (!p->u32_generic && p->log2N >= 12 && p->log2N <= 14) ? EPHDC_NTT_KERNEL_C5_U32

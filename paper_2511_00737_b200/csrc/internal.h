@@ -143,6 +143,9 @@ struct ephdc_ntt_plan {
     bool c5_alt_teams = false;   // EPHDC_NTT_ALT_TEAMS (A/B only)
     bool int_per_poly = false;   // EPHDC_NTT_ALT_TEAMS also selects the per-polynomial integer kernel (A/B)
     bool u32_generic = false;    // EPHDC_NTT_U32_GENERIC: the general u32 kernels instead of ntt32_c5.cu (A/B)
+    // u64 words with every prime < 2^30 at N = 2^12 .. 2^14: the ntt32_c5.cu kernels on
+    // the low words (unless EPHDC_NTT_U32_GENERIC / FORCE_INT)
+    bool u32_for_u64 = false;
     // inverse: DIT table [L][N] (W[h + jj] = omega^-(N/2h) jj, entry 0 = (q, 1/q)), fused
     // level-12 scaling [L][NC/2][2] (sigma_r, sigma_r W[NC/2 + r]), sigma_r = N^-1 psi^-r;
     // c_loc = psi^-(NC/2); block constants c_k = psi^-(NC k) [L][8]
@@ -234,6 +237,8 @@ cudaError_t launch_ntt_c5(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t 
 // cudaErrorNotSupported elsewhere)
 cudaError_t launch_pack_intt_q32(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b0, uint32_t nbat,
                                  uint32_t *d_M, cudaStream_t st);
+cudaError_t launch_ntt32_c5_u64(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
+                                cudaStream_t st);
 // c5 u32 kernels (ntt32_c5.cu) at N = 2^12 .. 2^14; cudaErrorNotSupported elsewhere
 cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, bool inverse,
                             cudaStream_t st);

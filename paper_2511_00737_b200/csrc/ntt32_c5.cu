@@ -66,7 +66,16 @@ struct Args {
     const u32 *ninv;         // [L][2] (N^-1, Shoup)
     u32 q[kMaxL];
     u32 zero;                // 0: a runtime addend that keeps the butterfly sums 3-input IADD3s
+    u64 *polys64;            // IO64: [batch][L][N] u64 words (residues < 2^30)
 };
+
+EPHDC_D void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ephdc_async::smem_u32(dst)), "l"(src) : "memory");
+}
+// arrives on *bar once all of this thread's earlier cp.async copies have landed
+EPHDC_D void cp_async_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ephdc_async::smem_u32(bar)) : "memory");
+}
 
 EPHDC_D int sw(int e) { return e ^ (((e >> 5) & 7) << 2); }
 
@@ -215,9 +224,15 @@ struct FromSmem {
 };
 // (Load: the inverse's input element i of the row comes from load(i) instead of B --
 // the slot pack of the query path)
-template <int LG, bool INV, class Load = FromSmem>
-EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid, const Load &load = Load()) {
+struct RowToSmem {
+    EPHDC_D void operator()(const u32 (&)[32]) const {}
+};
+// (RowOut: the row's 32 results go to out(x) instead of back to B)
+template <int LG, bool INV, class Load = FromSmem, class RowOut = RowToSmem>
+EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid, const Load &load = Load(),
+                    const RowOut &rout = RowOut()) {
     constexpr bool kLoad = !std::is_same<Load, FromSmem>::value;
+    constexpr bool kRowOut = !std::is_same<RowOut, RowToSmem>::value;
     uint32_t r0[32], r1[32];
     ephdc_tmem::ldx<32>(tbase, r0);
     ephdc_tmem::ldx<32>(tbase + 32u, r1);
@@ -246,12 +261,24 @@ EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid, const Load
     } else {   // half-size 2^s, pair 32 - 2^(5-s) + v
         gs_subs<5, 0, 5>(x, [&](int s, int v) { return tpair(r0, r1, 32 - (32 >> s) + v); }, gs_shoup(pr));
     }
+    if constexpr (kRowOut) {
+        rout(x);
+    } else {
 #pragma unroll
-    for (int m = 0; m < 8; ++m)
-        *reinterpret_cast<uint4 *>(P + 4 * (m ^ g7)) = make_uint4(x[4 * m], x[4 * m + 1], x[4 * m + 2], x[4 * m + 3]);
+        for (int m = 0; m < 8; ++m)
+            *reinterpret_cast<uint4 *>(P + 4 * (m ^ g7)) = make_uint4(x[4 * m], x[4 * m + 1], x[4 * m + 2], x[4 * m + 3]);
+    }
 }
 
-template <int LG, bool INV, bool OCC>
+// IO64: u64 words (every residue < 2^30).  TMA cannot drop the high words into the
+// 128-byte swizzled rows, so every thread copies the low words of 32 elements with
+// 4-byte cp.async (lanes on consecutive elements) into the same swizzled u32 layout,
+// signalling the buffer's mbarrier (NT arrivals) -- issued two items ahead, after the
+// first barrier of the current item -- and results leave as zero-extended u64 with
+// lanes on consecutive elements: the inverse straight from pass A's registers, the
+// forward from B after pass C (storing each thread's 256-byte row from registers
+// measured 0.45 vs 0.54 of HBM at 2^13: uncoalesced).
+template <int LG, bool INV, bool OCC, bool IO64 = false>
 __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     k_ntt32_c5(const __grid_constant__ CUtensorMap map, const __grid_constant__ Args a) {
     constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5, kNB = nbuf<LG, OCC>();
@@ -264,12 +291,16 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     TwH *tws = reinterpret_cast<TwH *>(bufs + kNB * NC);
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0)
-        for (int b = 0; b < kNB; ++b) ephdc_async::mbar_init(&mbar[b], 1);
+        for (int b = 0; b < kNB; ++b) ephdc_async::mbar_init(&mbar[b], IO64 ? NT : 1);
     if (warp == 0) ephdc_tmem::alloc(&tmem_slot, tmem_cols<LG>());
     ephdc_tmem::fence_before_sync();
     __syncthreads();
     ephdc_tmem::fence_after_sync();
     const uint32_t tbase = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 64u;
+    auto poly64 = [&](u32 w) -> u64 * {   // item w's polynomial (prime-major items)
+        const u32 j = w / a.batch, b = w - j * a.batch;
+        return a.polys64 + (((size_t)b * a.L + j) << LG);
+    };
 
     const u32 w0 = (u32)((u64)a.items * blockIdx.x / gridDim.x), w1 = (u32)((u64)a.items * (blockIdx.x + 1) / gridDim.x);
     const u32 n = w1 - w0;
@@ -285,14 +316,26 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
 #pragma unroll
         for (int k = 0; k < kBoxes; ++k) tma_load(dst + k * kBox * 32, &map, y + k * kBox, bar);
     };
-    if (tid == 0)
-        for (u32 i = 0; i < (u32)kNB && i < n; ++i) issue(i);
+    auto issue64 = [&](u32 i) {   // every thread: the low words of elements tid + NT k
+        u32 *dst = bufs + (i % kNB) * NC;
+        const u32 *src = reinterpret_cast<const u32 *>(poly64(w0 + i));
+#pragma unroll
+        for (int k = 0; k < kE; ++k) cp_async4(dst + sw(tid + NT * k), src + 2 * (tid + NT * k));
+        cp_async_arrive(&mbar[i % kNB]);
+    };
+    if constexpr (IO64) {
+        for (u32 i = 0; i + 1 < (u32)kNB && i < n; ++i) issue64(i);
+    } else {
+        if (tid == 0)
+            for (u32 i = 0; i < (u32)kNB && i < n; ++i) issue(i);
+    }
 
     u32 jcur = 0xffffffffu;
     Prime pr{0, 0, a.zero, {0, 0}, {0, 0}};
     for (u32 i = 0; i < n; ++i) {
         const u32 w = w0 + i, j = w / a.batch;
         if (j != jcur) {   // the previous item's last barrier freed the twiddles
+            if constexpr (IO64) __syncthreads();   // (IO64 items end without one)
             const TwPair<u32> *gt = a.tw + ((size_t)j << LG);
             for (int p = tid; p < NTW; p += NT) tws[p] = gt[p];
             uint32_t r[16];
@@ -332,6 +375,30 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
         }
         u32 *B = bufs + (i % kNB) * NC;
         ephdc_async::mbar_wait(&mbar[i % kNB], (i / kNB) & 1);
+        if constexpr (IO64) {
+            // the buffer of item i + kNB - 1 was last read by item i - 1, which every thread
+            // has left once the first barrier of item i is passed
+            u64 *o = poly64(w);
+            if constexpr (!INV) {
+                pass_a<LG, false>(B, tws, pr, tid);
+                __syncthreads();
+                if (i + kNB - 1 < n) issue64(i + kNB - 1);
+                pass_b<LG, false>(B, tws, pr, tid);
+                __syncthreads();
+                pass_c<LG, false>(B, tbase, pr, tid);
+                __syncthreads();   // rows back in B; stores with lanes on consecutive elements
+#pragma unroll
+                for (int k = 0; k < kE; ++k) __stcs(o + tid + NT * k, (unsigned long long)B[sw(tid + NT * k)]);
+            } else {
+                pass_c<LG, true>(B, tbase, pr, tid);
+                __syncthreads();
+                if (i + kNB - 1 < n) issue64(i + kNB - 1);
+                pass_b<LG, true>(B, tws, pr, tid);
+                __syncthreads();
+                pass_a<LG, true>(B, tws, pr, tid, [&](int e, u32 y) { __stcs(o + e, (unsigned long long)y); });
+            }
+            continue;
+        }
         if constexpr (!INV) {
             pass_a<LG, false>(B, tws, pr, tid);
             __syncthreads();
@@ -358,7 +425,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
             }
         }
     }
-    if (tid == 0) bulk_wait0();
+    if (!IO64 && tid == 0) bulk_wait0();
     ephdc_tmem::fence_before_sync();
     __syncthreads();
     ephdc_tmem::fence_after_sync();
@@ -466,17 +533,20 @@ bool make_map32(CUtensorMap *m, const void *base, uint64_t n_words, uint32_t box
 }
 
 template <int LG, bool INV>
-cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cudaStream_t st) {
+cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStream_t st, bool u64_words = false) {
     // inverse: the OCC form (two buffers, 3 / 6 CTAs per SM at 2^13 / 2^12: 0.546 vs
     // 0.531 of HBM at 2^13); forward: three buffers (0.525 vs 0.526; r47).
     // EPHDC_NTT_ALT_TEAMS swaps the forms (A/B).
-    const bool occ = INV != p->c5_alt_teams;
-    auto kern = occ ? k_ntt32_c5<LG, INV, true> : k_ntt32_c5<LG, INV, false>;
+    // u64 words: the IO64 form (three buffers, cp.async in, u64 stores out)
+    const bool occ = !u64_words && (INV != p->c5_alt_teams);
+    auto kern = u64_words ? k_ntt32_c5<LG, INV, false, true>
+                : occ     ? k_ntt32_c5<LG, INV, true> : k_ntt32_c5<LG, INV, false>;
     const size_t smem = occ ? smem_bytes<LG, true>() : smem_bytes<LG, false>();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    CUtensorMap map;
-    if (!make_map32(&map, polys, (uint64_t)batch * p->L * p->N, (uint32_t)box_rows<LG>())) return cudaErrorNotSupported;
+    CUtensorMap map{};
+    const uint64_t n = (uint64_t)batch * p->L * p->N;
+    if (!u64_words && !make_map32(&map, polys, n, (uint32_t)box_rows<LG>())) return cudaErrorNotSupported;
     Args a{};
     a.L = p->L;
     a.batch = batch;
@@ -485,6 +555,7 @@ cudaError_t launch(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, cud
     a.ninv = p->ninv32;
     for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
     a.zero = 0;
+    a.polys64 = u64_words ? static_cast<u64 *>(polys) : nullptr;
     const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * (occ ? cps<LG, true>() : cps<LG, false>()), a.items));
     kern<<<units, nthreads<LG>(), smem, st>>>(map, a);
     return counted(cudaGetLastError());
@@ -504,6 +575,21 @@ cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t
         case 12: return inverse ? launch<12, true>(p, d_polys, batch, st) : launch<12, false>(p, d_polys, batch, st);
         case 13: return inverse ? launch<13, true>(p, d_polys, batch, st) : launch<13, false>(p, d_polys, batch, st);
         case 14: return inverse ? launch<14, true>(p, d_polys, batch, st) : launch<14, false>(p, d_polys, batch, st);
+    }
+    return cudaErrorNotSupported;
+}
+
+// u64 words, every prime < 2^30 (residues < q: the high words are zero and stay zero)
+cudaError_t launch_ntt32_c5_u64(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
+                                cudaStream_t st) {
+    if (!p->u32_for_u64 || !p->tw32) return cudaErrorNotSupported;
+    if (batch == 0) return cudaSuccess;
+    if ((uint64_t)batch * p->L > 0xffffffffull || ((uintptr_t)d_polys & 15)) return cudaErrorNotSupported;
+    using namespace c5u32;
+    switch (p->log2N) {
+        case 12: return inverse ? launch<12, true>(p, d_polys, batch, st, true) : launch<12, false>(p, d_polys, batch, st, true);
+        case 13: return inverse ? launch<13, true>(p, d_polys, batch, st, true) : launch<13, false>(p, d_polys, batch, st, true);
+        case 14: return inverse ? launch<14, true>(p, d_polys, batch, st, true) : launch<14, false>(p, d_polys, batch, st, true);
     }
     return cudaErrorNotSupported;
 }

@@ -241,3 +241,30 @@ def test_ntt_c5_u32_stress_repeated_launches():
             assert torch.equal(d, g), (it, log2N, L, batch)
         eph.ntt_inv32(pc, d)
         assert torch.equal(d, x), (it, log2N, L, batch)
+
+
+@pytest.mark.parametrize("log2N", [12, 13, 14])
+@pytest.mark.parametrize("L,batch", [(1, 1), (3, 7), (16, 3), (2, 301)])
+def test_ntt_u64_words_30bit_on_u32_kernels(log2N, L, batch):
+    """u64 words with every prime < 2^30 run the u32 kernels on the low words (TMA with
+    element stride 2): = the FP64 c5 kernels (EPHDC_NTT_U32_GENERIC keeps those) bit for
+    bit, = the oracle on sampled polynomials, high words stay zero, inverse round-trips."""
+    N = 1 << log2N
+    q = nt.prime_chain([30] * L, log2N)
+    x = inp.gen_residues(q, batch, N, seed=5000 + 7 * log2N + L + batch)
+    pa, pb = eph.NttPlan(q, log2N), eph.NttPlan(q, log2N, u32_generic=True)
+    assert pa.fwd_kernel == pa.inv_kernel == "c5_u32" and pb.fwd_kernel == "c5_f64"
+    da, db = _dev(x), _dev(x)
+    eph.ntt_fwd(pa, da)
+    eph.ntt_fwd(pb, db)
+    assert torch.equal(da, db)
+    got = _host(da)
+    assert int(got.max()) < (1 << 30)
+    for b in sorted({0, batch - 1}):
+        for j in range(L):
+            psi = nt.min_primitive_2n_root(q[j], N)
+            assert np.array_equal(got[b, j], core.ntt_fwd(x[b, j][None, :], log2N, q[j], psi)[0]), (b, j)
+    eph.ntt_inv(pa, da)
+    eph.ntt_inv(pb, db)
+    assert torch.equal(da, db)
+    assert np.array_equal(_host(da), x)
