@@ -388,7 +388,11 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
                 pass_c<LG, false>(B, tbase, pr, tid);
                 __syncthreads();   // rows back in B; stores with lanes on consecutive elements
 #pragma unroll
-                for (int k = 0; k < kE; ++k) __stcs(o + tid + NT * k, (unsigned long long)B[sw(tid + NT * k)]);
+                for (int k = 0; k < kE / 2; ++k) {   // pairs (e, e + 1): sw keeps them adjacent
+                    const int e = 2 * (tid + NT * k);
+                    const uint2 v = *reinterpret_cast<const uint2 *>(B + sw(e));
+                    __stcs(reinterpret_cast<ulonglong2 *>(o + e), make_ulonglong2(v.x, v.y));
+                }
             } else {
                 pass_c<LG, true>(B, tbase, pr, tid);
                 __syncthreads();
