@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """profiles/ncu_metrics.json entry for one config from an `ncu --set full` capture of the
-bench command (kernels k_ntt_mac_f64 / k_ntt_mac, k_pack_intt_q, k_encode_tc):
+bench command (kernels k_ntt_mac_f64 / k_ntt_mac, k_pack_intt32 / k_pack_intt_q, k_encode_tc):
   fused pass: DRAM bytes, duration, GB/s, FP64-pipe and integer-pipe utilisation;
   pack + INTT_t: integer-pipe (alu + fma) utilisation, duration;
   encoder: tensor-pipe utilisation, duration.
@@ -51,7 +51,7 @@ def main():
                             "fp64_pipe_pct": f(k["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]),
                             "alu_pipe_pct": f(k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]),
                             "dram_throughput_pct": f(k["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"])}
-        elif "k_pack_intt_q" in name and "pack" not in out:
+        elif "k_pack_intt" in name and "pack" not in out:
             out["pack"] = {"kernel": name.split("(")[0], "duration_ms": ms,
                            "alu_pipe_pct": f(k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]),
                            "fma_pipe_pct": f(k["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"]),
