@@ -67,6 +67,7 @@ struct Args {
     u32 q[kMaxL];
     u32 zero;                // 0: a runtime addend that keeps the butterfly sums 3-input IADD3s
     u64 *polys64;            // IO64: [batch][L][N] u64 words (residues < 2^30)
+    u32 *polys32;            // DOUT: the u32 words (results stored from the last pass)
 };
 
 EPHDC_D void cp_async4(void *dst, const void *src) {
@@ -278,7 +279,11 @@ EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid, const Load
 // lanes on consecutive elements: the inverse straight from pass A's registers, the
 // forward from B after pass C (storing each thread's 256-byte row from registers
 // measured 0.45 vs 0.54 of HBM at 2^13: uncoalesced).
-template <int LG, bool INV, bool OCC, bool IO64 = false>
+// DOUT (u32 words): TMA in, but results stored by the threads -- the inverse from pass
+// A's registers (lanes on consecutive elements), the forward by each warp from its own
+// rows after pass C (16-byte stores, lanes on consecutive chunks) -- so no item ends with
+// a CTA barrier; the load of item i + kNB - 1 is issued after item i's first barrier.
+template <int LG, bool INV, bool OCC, bool IO64 = false, bool DOUT = false>
 __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     k_ntt32_c5(const __grid_constant__ CUtensorMap map, const __grid_constant__ Args a) {
     constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5, kNB = nbuf<LG, OCC>();
@@ -325,6 +330,9 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     };
     if constexpr (IO64) {
         for (u32 i = 0; i + 1 < (u32)kNB && i < n; ++i) issue64(i);
+    } else if constexpr (DOUT) {
+        if (tid == 0)
+            for (u32 i = 0; i + 1 < (u32)kNB && i < n; ++i) issue(i);
     } else {
         if (tid == 0)
             for (u32 i = 0; i < (u32)kNB && i < n; ++i) issue(i);
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     for (u32 i = 0; i < n; ++i) {
         const u32 w = w0 + i, j = w / a.batch;
         if (j != jcur) {   // the previous item's last barrier freed the twiddles
-            if constexpr (IO64) __syncthreads();   // (IO64 items end without one)
+            if constexpr (IO64 || DOUT) __syncthreads();   // (these items end without one)
             const TwPair<u32> *gt = a.tw + ((size_t)j << LG);
             for (int p = tid; p < NTW; p += NT) tws[p] = gt[p];
             uint32_t r[16];
@@ -386,10 +394,13 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
                 pass_b<LG, false>(B, tws, pr, tid);
                 __syncthreads();
                 pass_c<LG, false>(B, tbase, pr, tid);
-                __syncthreads();   // rows back in B; stores with lanes on consecutive elements
+                // rows back in B; warp w's rows are elements [1024 w, 1024 w + 1024), stored
+                // by the same warp with lanes on consecutive pairs: a warp barrier suffices
+                __syncwarp();
+                const int eb = 1024 * warp + 2 * (tid & 31);
 #pragma unroll
                 for (int k = 0; k < kE / 2; ++k) {   // pairs (e, e + 1): sw keeps them adjacent
-                    const int e = 2 * (tid + NT * k);
+                    const int e = eb + 64 * k;
                     const uint2 v = *reinterpret_cast<const uint2 *>(B + sw(e));
                     __stcs(reinterpret_cast<ulonglong2 *>(o + e), make_ulonglong2(v.x, v.y));
                 }
@@ -400,6 +411,38 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
                 pass_b<LG, true>(B, tws, pr, tid);
                 __syncthreads();
                 pass_a<LG, true>(B, tws, pr, tid, [&](int e, u32 y) { __stcs(o + e, (unsigned long long)y); });
+            }
+            continue;
+        }
+        if constexpr (DOUT) {
+            u32 *o = a.polys32 + ((size_t)(w - j * a.batch) * a.L + j) * NC;
+            auto reissue = [&]() {   // item i - 1's buffer is free behind item i's first barrier
+                if (tid == 0 && i + kNB - 1 < n) {
+                    ephdc_async::fence_proxy_async();
+                    issue(i + kNB - 1);
+                }
+            };
+            if constexpr (!INV) {
+                pass_a<LG, false>(B, tws, pr, tid);
+                __syncthreads();
+                reissue();
+                pass_b<LG, false>(B, tws, pr, tid);
+                __syncthreads();
+                pass_c<LG, false>(B, tbase, pr, tid);
+                __syncwarp();   // warp w's rows = words [1024 w, 1024 w + 1024)
+                const int eb = 1024 * warp + 4 * (tid & 31);
+#pragma unroll
+                for (int k = 0; k < kE / 4; ++k) {
+                    const int e = eb + 128 * k;
+                    __stcs(reinterpret_cast<uint4 *>(o + e), *reinterpret_cast<const uint4 *>(B + sw(e)));
+                }
+            } else {
+                pass_c<LG, true>(B, tbase, pr, tid);
+                __syncthreads();
+                reissue();
+                pass_b<LG, true>(B, tws, pr, tid);
+                __syncthreads();
+                pass_a<LG, true>(B, tws, pr, tid, [&](int e, u32 y) { __stcs(o + e, y); });
             }
             continue;
         }
@@ -429,7 +472,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
             }
         }
     }
-    if (!IO64 && tid == 0) bulk_wait0();
+    if (!IO64 && !DOUT && tid == 0) bulk_wait0();
     ephdc_tmem::fence_before_sync();
     __syncthreads();
     ephdc_tmem::fence_after_sync();
@@ -542,9 +585,15 @@ cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStr
     // 0.531 of HBM at 2^13); forward: three buffers (0.525 vs 0.526; r47).
     // EPHDC_NTT_ALT_TEAMS swaps the forms (A/B).
     // u64 words: the IO64 form (three buffers, cp.async in, u64 stores out)
-    const bool occ = !u64_words && (INV != p->c5_alt_teams);
+    // u32 words: the inverse stores from pass A's registers (DOUT: 0.551 / 0.511 vs 0.547
+    // / 0.494 of HBM with the TMA store at 2^13 / 2^14), the forward keeps the TMA store
+    // (0.527 / 0.498 vs 0.511 / 0.472 with per-warp 16-byte stores; r57).
+    // EPHDC_NTT_ALT_TEAMS swaps the forms (A/B).
+    const bool occ = !u64_words && INV;
+    const bool dout = INV != p->c5_alt_teams;
     auto kern = u64_words ? k_ntt32_c5<LG, INV, false, true>
-                : occ     ? k_ntt32_c5<LG, INV, true> : k_ntt32_c5<LG, INV, false>;
+                : occ     ? (dout ? k_ntt32_c5<LG, INV, true, false, true> : k_ntt32_c5<LG, INV, true>)
+                          : (dout ? k_ntt32_c5<LG, INV, false, false, true> : k_ntt32_c5<LG, INV, false>);
     const size_t smem = occ ? smem_bytes<LG, true>() : smem_bytes<LG, false>();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -560,6 +609,7 @@ cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStr
     for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
     a.zero = 0;
     a.polys64 = u64_words ? static_cast<u64 *>(polys) : nullptr;
+    a.polys32 = u64_words ? nullptr : static_cast<u32 *>(polys);
     const uint32_t units = std::max<uint32_t>(1, std::min<uint32_t>(148u * (occ ? cps<LG, true>() : cps<LG, false>()), a.items));
     kern<<<units, nthreads<LG>(), smem, st>>>(map, a);
     return counted(cudaGetLastError());
