@@ -117,7 +117,8 @@ typedef struct {
                           * 1-3 also select a one-team variant); bit 6 = the two-group
                           * kernel at N = 2^14 (default there: one team); bit 7 = the
                           * round-1 slot pack + INTT_t kernel (default at N >= 2^12:
-                          * the ntt32_c5.cu passes)                                   */
+                          * the ntt32_c5.cu passes); bit 8 = that kernel without the
+                          * L1 prefetch of the next row's query bytes                 */
     uint32_t bg;         /* FP64 fused kernel: batches per group (0 = planner)       */
     uint32_t G;          /* FP64 fused kernel: dims per chunk (0 = planner)          */
     uint32_t m_batches;  /* batches of encoded plaintexts kept (0 = planner: all of

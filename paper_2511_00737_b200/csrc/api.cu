@@ -651,7 +651,7 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
             const uint32_t g = std::min(ws->m_batches, nb - b0);
             {
                 Timer tm(ws, st, kClsPack);
-                EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b0, g, 0, c->p.D_live, ws->d_M, st, (ws->plan.flags & 128u) != 0));
+                EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b0, g, 0, c->p.D_live, ws->d_M, st, ws->plan.flags));
                 tm.done();
             }
             {
@@ -670,7 +670,7 @@ static ephdc_status infer_impl(const ephdc_ctx *c, const ephdc_model *m, ephdc_w
     for (uint32_t b = 0; b < nb; ++b) {
         {
             Timer tm(ws, st, kClsPack);
-            EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, 1, 0, c->p.D_live, ws->d_M, st, (ws->plan.flags & 128u) != 0));
+            EPHDC_CUDA_TRY(launch_pack_intt_queries(c, d_H, nq, b, 1, 0, c->p.D_live, ws->d_M, st, ws->plan.flags));
             tm.done();
         }
         {

@@ -162,7 +162,7 @@ cudaError_t launch_encode(const ephdc_ctx *c, const void *d_X, const int8_t *d_P
                           cudaStream_t st);
 // slot pack + INTT_t of batches [b, b+nbat) x dims [d0, d0+nd) -> d_M [nbat][nd][N]
 cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t nbat,
-                                     uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st, bool alt = false);
+                                     uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st, uint32_t plan_flags = 0);
 cudaError_t launch_pack_intt_model(const ephdc_ctx *c, const int8_t *d_C, uint32_t d0, uint32_t nd, uint32_t *d_M,
                                    cudaStream_t st);
 cudaError_t launch_ntt_mac(const ephdc_ctx *c, const uint32_t *d_M, const uint64_t *d_model, uint64_t *d_out,
@@ -236,7 +236,7 @@ cudaError_t launch_ntt_c5(const ephdc_ntt_plan *pl, uint64_t *d_polys, uint32_t 
 // query-path slot pack + INTT_t on the ntt32_c5.cu passes (N = 2^12 .. 2^14;
 // cudaErrorNotSupported elsewhere)
 cudaError_t launch_pack_intt_q32(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b0, uint32_t nbat,
-                                 uint32_t *d_M, cudaStream_t st);
+                                 uint32_t *d_M, cudaStream_t st, bool no_prefetch = false);
 cudaError_t launch_ntt32_c5_u64(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
                                 cudaStream_t st);
 // c5 u32 kernels (ntt32_c5.cu) at N = 2^12 .. 2^14; cudaErrorNotSupported elsewhere

@@ -966,13 +966,14 @@ static cudaError_t packq_launch(const ephdc_ctx *c, const int8_t *H, u32 nq, u32
 }
 
 cudaError_t launch_pack_intt_queries(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b, uint32_t nbat,
-                                     uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st, bool alt) {
+                                     uint32_t d0, uint32_t nd, uint32_t *d_M, cudaStream_t st, uint32_t plan_flags) {
+    const bool alt = (plan_flags & 128u) != 0, no_pf = (plan_flags & 256u) != 0;
     // whole-dimension calls (the hot path) use the persistent kernels -- at N >= 2^12 the
     // ntt32_c5.cu passes (alt: the round-1 kernel, A/B) -- partial ranges (the parity
     // export of single dims) the one-CTA-per-row kernel
     if (d0 == 0 && nd == c->p.D_live && nbat > 0 && nd > 0) {
         if (!alt) {
-            const cudaError_t e = launch_pack_intt_q32(c, d_H, nq, b, nbat, d_M, st);
+            const cudaError_t e = launch_pack_intt_q32(c, d_H, nq, b, nbat, d_M, st, no_pf);
             if (e != cudaErrorNotSupported) return e;
         }
         switch (c->p.log2N) {

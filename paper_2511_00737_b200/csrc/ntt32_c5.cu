@@ -492,7 +492,7 @@ struct PackArgs32 {
     const TwPair<u32> *itw;   // [N] psiinv_rev mod t, Shoup pairs
 };
 
-template <int LG>
+template <int LG, bool PF = true>
 __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
     k_pack_intt32(const int8_t *__restrict__ H, PackArgs32 a, u32 *__restrict__ M) {
     constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5;
@@ -548,6 +548,14 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
         };
         pass_c<LG, true>(B, tbase, pr, tid, load);
         __syncthreads();
+        if constexpr (PF) {   // the next row's H bytes of this thread's slots toward L2 / L1
+            const u32 rn = row + gridDim.x;
+            if (rn < rows) {
+                const u32 bbn = rn / a.D, dn = rn - bbn * a.D;
+                const u32 q0 = a.k == 1u ? 32u * tid : __umulhi(32u * tid, a.kmagic);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(H + (size_t)dn * a.nq + (size_t)(a.b0 + bbn) * a.B + q0));
+            }
+        }
         pass_b<LG, true>(B, tws, pr, tid);
         __syncthreads();
         u32 *o = M + (size_t)row * NC;
@@ -650,7 +658,7 @@ cudaError_t launch_ntt32_c5_u64(const ephdc_ntt_plan *p, uint64_t *d_polys, uint
 
 // Slot pack + INTT_t of the query path at N = 2^12 .. 2^14 (cudaErrorNotSupported below).
 cudaError_t launch_pack_intt_q32(const ephdc_ctx *c, const int8_t *d_H, uint32_t nq, uint32_t b0, uint32_t nbat,
-                                 uint32_t *d_M, cudaStream_t st) {
+                                 uint32_t *d_M, cudaStream_t st, bool no_prefetch) {
     using namespace c5u32;
     PackArgs32 a{};
     a.t = (u32)c->t;
@@ -676,9 +684,9 @@ cudaError_t launch_pack_intt_q32(const ephdc_ctx *c, const int8_t *d_H, uint32_t
         return counted(cudaGetLastError());
     };
     switch (c->p.log2N) {
-        case 12: return go(k_pack_intt32<12>, 12);
-        case 13: return go(k_pack_intt32<13>, 13);
-        case 14: return go(k_pack_intt32<14>, 14);
+        case 12: return no_prefetch ? go(k_pack_intt32<12, false>, 12) : go(k_pack_intt32<12, true>, 12);
+        case 13: return no_prefetch ? go(k_pack_intt32<13, false>, 13) : go(k_pack_intt32<13, true>, 13);
+        case 14: return no_prefetch ? go(k_pack_intt32<14, false>, 14) : go(k_pack_intt32<14, true>, 14);
     }
     return cudaErrorNotSupported;
 }

@@ -42,6 +42,7 @@ VARIANTS = [
     {"flags": 64},           # the two-group kernel at N = 2^14 (c4; one team by default)
     {"flags": 64, "bg": 1, "G": 37},
     {"flags": 128},          # the round-1 slot pack + INTT_t kernel (default: ntt32_c5.cu passes)
+    {"flags": 256},          # the ntt32_c5.cu pack without the next-row prefetch
 ]
 
 
