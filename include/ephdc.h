@@ -428,8 +428,10 @@ ephdc_status ephdc_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const ui
 #define EPHDC_NTT_KERNEL_INT 0u     /* integer pipe, u64 Shoup (any prime < 2^61)          */
 #define EPHDC_NTT_KERNEL_F64 1u     /* FP64 pipe, per-polynomial CTAs (round-1 kernels)    */
 #define EPHDC_NTT_KERNEL_C5_F64 2u  /* FP64 pipe, persistent TMA-fed kernels (ntt_c5.cu)   */
-#define EPHDC_NTT_KERNEL_C5_U32 3u  /* integer pipe, u32 words, persistent TMA-fed kernels
-                                       (ntt32_c5.cu; N = 2^12 .. 2^14)                   */
+#define EPHDC_NTT_KERNEL_C5_U32 3u  /* integer pipe, persistent TMA-fed u32 kernels
+                                       (ntt32_c5.cu; u32 words N = 2^12 .. 2^16 -- 2^15 /
+                                       2^16 as global stages + 2^14 slices; u64 words
+                                       with primes < 2^30 N = 2^12 .. 2^14)              */
 typedef struct {
     uint32_t fwd_kernel, inv_kernel;  /* EPHDC_NTT_KERNEL_* of ephdc_ntt_fwd / _inv       */
     uint32_t u32_words;               /* 1 if the *32 entry points are available          */

@@ -1160,7 +1160,7 @@ ephdc_status ephdc_ntt_plan_query(const ephdc_ntt_plan *p, ephdc_ntt_plan_info *
                                       : EPHDC_NTT_KERNEL_INT;
     info->u32_words = p->tw32 != nullptr;
     info->u32_kernel = !p->tw32 ? EPHDC_NTT_KERNEL_INT
-                       : (!p->u32_generic && p->log2N >= 12 && p->log2N <= 14) ? EPHDC_NTT_KERNEL_C5_U32
+                       : (!p->u32_generic && p->log2N >= 12) ? EPHDC_NTT_KERNEL_C5_U32
                                                                                : EPHDC_NTT_KERNEL_INT;
     return EPHDC_OK;
 }

@@ -239,7 +239,10 @@ cudaError_t launch_pack_intt_q32(const ephdc_ctx *c, const int8_t *d_H, uint32_t
                                  uint32_t *d_M, cudaStream_t st, bool no_prefetch = false);
 cudaError_t launch_ntt32_c5_u64(const ephdc_ntt_plan *p, uint64_t *d_polys, uint32_t batch, bool inverse,
                                 cudaStream_t st);
-// c5 u32 kernels (ntt32_c5.cu) at N = 2^12 .. 2^14; cudaErrorNotSupported elsewhere
+cudaError_t launch_ntt_global32(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, bool inverse,
+                                cudaStream_t st);
+// c5 u32 kernels (ntt32_c5.cu) at N = 2^12 .. 2^16 (2^15 / 2^16: global stages + 2^14
+// slices); cudaErrorNotSupported elsewhere
 cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t batch, bool inverse,
                             cudaStream_t st);
 bool plan_f64(const std::vector<uint64_t> &q, uint64_t t, uint32_t log2N, F64Plan *plan);

@@ -1182,6 +1182,15 @@ static cudaError_t nttg_launch(const ephdc_ntt_plan *p, W *polys, u32 batch, cud
     return counted(cudaGetLastError());
 }
 
+// The GS = log2(N) - 14 global stages alone on u32 words (the ntt32_c5.cu slice kernels
+// do the 2^14-point rest): forward first, inverse last (with N^-1).
+cudaError_t launch_ntt_global32(const ephdc_ntt_plan *p, uint32_t *polys, uint32_t batch, bool inverse,
+                                cudaStream_t st) {
+    if (p->log2N == 15) return inverse ? nttg_launch<1, true, u32>(p, polys, batch, st) : nttg_launch<1, false, u32>(p, polys, batch, st);
+    if (p->log2N == 16) return inverse ? nttg_launch<2, true, u32>(p, polys, batch, st) : nttg_launch<2, false, u32>(p, polys, batch, st);
+    return cudaErrorNotSupported;
+}
+
 template <bool INV, typename W>
 static cudaError_t ntt_large(const ephdc_ntt_plan *p, W *polys, u32 batch, cudaStream_t st) {
     // forward: global stages, then 2^14-point slices; inverse: slices, then global stages

@@ -68,6 +68,7 @@ struct Args {
     u32 zero;                // 0: a runtime addend that keeps the butterfly sums 3-input IADD3s
     u64 *polys64;            // IO64: [batch][L][N] u64 words (residues < 2^30)
     u32 *polys32;            // DOUT: the u32 words (results stored from the last pass)
+    u32 slog;                // log2 of the slices per polynomial (N = NC << slog): items (prime, slice, poly)
 };
 
 EPHDC_D void cp_async4(void *dst, const void *src) {
@@ -160,7 +161,7 @@ struct ToSmem {
     EPHDC_D void operator()(int, u32) const {}
 };
 // (Out: the inverse's output element e goes to out(e, value) instead of B)
-template <int LG, bool INV, class Out = ToSmem>
+template <int LG, bool INV, bool FUSE = true, class Out = ToSmem>
 EPHDC_D void pass_a(u32 *B, const TwH *tws, const Prime &pr, int tid, const Out &out = Out()) {
     constexpr bool kOut = !std::is_same<Out, ToSmem>::value;
     constexpr int NC = 1 << LG, NT = NC / kE, RA = LG - 9, R = 1 << RA, GA = kE / R;
@@ -175,11 +176,17 @@ EPHDC_D void pass_a(u32 *B, const TwH *tws, const Prime &pr, int tid, const Out 
         } else {   // half-sizes 2^(9+sub): psiinv_rev[NC/2^(10+sub) + v]; the last one fused with N^-1
             gs_subs<RA, 0, RA - 1>(x, [&](int sub, int v) { return tws[(NC >> (10 + sub)) + v]; }, gs_ab(pr));
             constexpr int hs = R / 2;
+            if constexpr (FUSE) {
 #pragma unroll
-            for (int kk = 0; kk < hs; ++kk) {
-                const u32 X = x[kk], Y = x[kk + hs];
-                x[kk] = csub(mul_shoup_lazy<u32>(X + Y, pr.ninv.w, pr.ninv.wp, pr.q), pr.q);
-                x[kk + hs] = csub(mul_shoup_lazy<u32>(X - Y + pr.two_q, pr.wn.w, pr.wn.wp, pr.q), pr.q);
+                for (int kk = 0; kk < hs; ++kk) {
+                    const u32 X = x[kk], Y = x[kk + hs];
+                    x[kk] = csub(mul_shoup_lazy<u32>(X + Y, pr.ninv.w, pr.ninv.wp, pr.q), pr.q);
+                    x[kk + hs] = csub(mul_shoup_lazy<u32>(X - Y + pr.two_q, pr.wn.w, pr.wn.wp, pr.q), pr.q);
+                }
+            } else {   // a slice: the last local level is a plain GS level (lazy [0, 2q) out)
+                const TwPair<u32> t = tws[1];
+#pragma unroll
+                for (int kk = 0; kk < hs; ++kk) gs_ab(pr)(x[kk], x[kk + hs], t);
             }
         }
         if constexpr (kOut) {
@@ -283,7 +290,9 @@ EPHDC_D void pass_c(u32 *B, uint32_t tbase, const Prime &pr, int tid, const Load
 // A's registers (lanes on consecutive elements), the forward by each warp from its own
 // rows after pass C (16-byte stores, lanes on consecutive chunks) -- so no item ends with
 // a CTA barrier; the load of item i + kNB - 1 is issued after item i's first barrier.
-template <int LG, bool INV, bool OCC, bool IO64 = false, bool DOUT = false>
+// SLC: the CTA transforms 2^LG-point slices of a 2^(LG + slog)-point transform whose
+// global stages run in k_ntt_global (N^-1 applied there, not in pass A).
+template <int LG, bool INV, bool OCC, bool IO64 = false, bool DOUT = false, bool SLC = false>
 __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     k_ntt32_c5(const __grid_constant__ CUtensorMap map, const __grid_constant__ Args a) {
     constexpr int NC = 1 << LG, NT = NC / kE, NTW = NC >> 5, kNB = nbuf<LG, OCC>();
@@ -295,6 +304,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     u32 *bufs = reinterpret_cast<u32 *>(smem_raw + ((1024u - (ephdc_async::smem_u32(smem_raw) & 1023u)) & 1023u));
     TwH *tws = reinterpret_cast<TwH *>(bufs + kNB * NC);
     const int tid = threadIdx.x, warp = tid >> 5;
+    const u32 slog_ = SLC ? a.slog : 0u;
     if (tid == 0)
         for (int b = 0; b < kNB; ++b) ephdc_async::mbar_init(&mbar[b], IO64 ? NT : 1);
     if (warp == 0) ephdc_tmem::alloc(&tmem_slot, tmem_cols<LG>());
@@ -302,17 +312,17 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     __syncthreads();
     ephdc_tmem::fence_after_sync();
     const uint32_t tbase = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 64u;
-    auto poly64 = [&](u32 w) -> u64 * {   // item w's polynomial (prime-major items)
-        const u32 j = w / a.batch, b = w - j * a.batch;
-        return a.polys64 + (((size_t)b * a.L + j) << LG);
+    // items are (prime j, slice s, polynomial b), b fastest: segment js = j 2^slog + s
+    auto elem_off = [&](u32 w) -> size_t {   // first element of item w
+        const u32 js = w / a.batch, b = w - js * a.batch;
+        const u32 j = js >> slog_, sl = js & ((1u << slog_) - 1u);
+        return ((((size_t)b * a.L + j) << slog_) + sl) << LG;
     };
+    auto poly64 = [&](u32 w) -> u64 * { return a.polys64 + elem_off(w); };
 
     const u32 w0 = (u32)((u64)a.items * blockIdx.x / gridDim.x), w1 = (u32)((u64)a.items * (blockIdx.x + 1) / gridDim.x);
     const u32 n = w1 - w0;
-    auto row_of = [&](u32 w) -> int {   // first 128-byte row of item w (prime-major items)
-        const u32 j = w / a.batch, b = w - j * a.batch;
-        return (int)((((size_t)b * a.L + j) << LG) >> 5);
-    };
+    auto row_of = [&](u32 w) -> int { return (int)(elem_off(w) >> 5); };   // first 128-byte row
     auto issue = [&](u32 i) {   // one thread
         uint64_t *bar = &mbar[i % kNB];
         u32 *dst = bufs + (i % kNB) * NC;
@@ -341,11 +351,19 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
     u32 jcur = 0xffffffffu;
     Prime pr{0, 0, a.zero, {0, 0}, {0, 0}};
     for (u32 i = 0; i < n; ++i) {
-        const u32 w = w0 + i, j = w / a.batch;
-        if (j != jcur) {   // the previous item's last barrier freed the twiddles
+        const u32 w = w0 + i, js = w / a.batch, j = js >> slog_;
+        if (js != jcur) {   // the previous item's last barrier freed the twiddles
             if constexpr (IO64 || DOUT) __syncthreads();   // (these items end without one)
-            const TwPair<u32> *gt = a.tw + ((size_t)j << LG);
-            for (int p = tid; p < NTW; p += NT) tws[p] = gt[p];
+            const TwPair<u32> *gt = a.tw + ((size_t)j << (LG + slog_));
+            // slice sl of S = 2^slog: the local table entry m + B (m a power of two) is the
+            // global entry (S + sl) m + B (S = 1: the identity)
+            const u32 ssl = (1u << slog_) + (js & ((1u << slog_) - 1u));
+            auto glob = [&](int idx) -> int {
+                const int m = 1 << (31 - __clz(idx));
+                return (int)ssl * m + (idx - m);
+            };
+            for (int p = tid; p < NTW; p += NT)
+                if (p > 0) tws[p] = gt[glob(p)];
             uint32_t r[16];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -363,7 +381,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
                             const int v = p - (32 - (32 >> s));
                             idx = (NC >> (s + 1)) + (tid << (4 - s)) + v;
                         }
-                        t = gt[idx];
+                        t = gt[glob(idx)];
                     }
                     r[2 * c] = t.w;
                     r[2 * c + 1] = t.wp;
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
                 const u32 wv = (u32)(((u64)gt[1].w * pr.ninv.w) % pr.q);
                 pr.wn = TwPair<u32>{wv, (u32)(((u64)wv << 32) / pr.q)};
             }
-            jcur = j;
+            jcur = js;
             __syncthreads();
         }
         u32 *B = bufs + (i % kNB) * NC;
@@ -415,7 +433,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
             continue;
         }
         if constexpr (DOUT) {
-            u32 *o = a.polys32 + ((size_t)(w - j * a.batch) * a.L + j) * NC;
+            u32 *o = a.polys32 + elem_off(w);
             auto reissue = [&]() {   // item i - 1's buffer is free behind item i's first barrier
                 if (tid == 0 && i + kNB - 1 < n) {
                     ephdc_async::fence_proxy_async();
@@ -442,7 +460,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
                 reissue();
                 pass_b<LG, true>(B, tws, pr, tid);
                 __syncthreads();
-                pass_a<LG, true>(B, tws, pr, tid, [&](int e, u32 y) { __stcs(o + e, y); });
+                pass_a<LG, true, !SLC>(B, tws, pr, tid, [&](int e, u32 y) { __stcs(o + e, y); });
             }
             continue;
         }
@@ -457,7 +475,7 @@ __global__ void __launch_bounds__(nthreads<LG>(), cps<LG, OCC>())
             __syncthreads();
             pass_b<LG, true>(B, tws, pr, tid);
             __syncthreads();
-            pass_a<LG, true>(B, tws, pr, tid);
+            pass_a<LG, true, !SLC>(B, tws, pr, tid);
         }
         ephdc_async::fence_proxy_async();   // this thread's writes -> the TMA store
         __syncthreads();
@@ -588,7 +606,8 @@ bool make_map32(CUtensorMap *m, const void *base, uint64_t n_words, uint32_t box
 }
 
 template <int LG, bool INV>
-cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStream_t st, bool u64_words = false) {
+cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStream_t st, bool u64_words = false,
+                   uint32_t slog = 0) {
     // inverse: the OCC form (two buffers, 3 / 6 CTAs per SM at 2^13 / 2^12: 0.546 vs
     // 0.531 of HBM at 2^13); forward: three buffers (0.525 vs 0.526; r47).
     // EPHDC_NTT_ALT_TEAMS swaps the forms (A/B).
@@ -600,6 +619,7 @@ cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStr
     const bool occ = !u64_words && INV;
     const bool dout = INV != p->c5_alt_teams;
     auto kern = u64_words ? k_ntt32_c5<LG, INV, false, true>
+                : slog    ? (dout ? k_ntt32_c5<LG, INV, false, false, true, true> : k_ntt32_c5<LG, INV, false, false, false, true>)
                 : occ     ? (dout ? k_ntt32_c5<LG, INV, true, false, true> : k_ntt32_c5<LG, INV, true>)
                           : (dout ? k_ntt32_c5<LG, INV, false, false, true> : k_ntt32_c5<LG, INV, false>);
     const size_t smem = occ ? smem_bytes<LG, true>() : smem_bytes<LG, false>();
@@ -611,7 +631,8 @@ cudaError_t launch(const ephdc_ntt_plan *p, void *polys, uint32_t batch, cudaStr
     Args a{};
     a.L = p->L;
     a.batch = batch;
-    a.items = p->L * batch;
+    a.items = (p->L << slog) * batch;
+    a.slog = slog;
     a.tw = INV ? p->itw32 : p->tw32;
     a.ninv = p->ninv32;
     for (uint32_t j = 0; j < p->L; ++j) a.q[j] = (u32)p->q[j];
@@ -637,6 +658,18 @@ cudaError_t launch_ntt32_c5(const ephdc_ntt_plan *p, uint32_t *d_polys, uint32_t
         case 12: return inverse ? launch<12, true>(p, d_polys, batch, st) : launch<12, false>(p, d_polys, batch, st);
         case 13: return inverse ? launch<13, true>(p, d_polys, batch, st) : launch<13, false>(p, d_polys, batch, st);
         case 14: return inverse ? launch<14, true>(p, d_polys, batch, st) : launch<14, false>(p, d_polys, batch, st);
+        case 15:
+        case 16: {   // log2(N) - 14 global stages (one HBM pass) + 2^14-point slices
+            if (((uint64_t)batch * p->L << (p->log2N - 14)) > 0xffffffffull) return cudaErrorNotSupported;
+            const uint32_t slog = p->log2N - 14;
+            cudaError_t e;
+            if (!inverse) {
+                if ((e = launch_ntt_global32(p, d_polys, batch, false, st)) != cudaSuccess) return e;
+                return launch<14, false>(p, d_polys, batch, st, false, slog);
+            }
+            if ((e = launch<14, true>(p, d_polys, batch, st, false, slog)) != cudaSuccess) return e;
+            return launch_ntt_global32(p, d_polys, batch, true, st);
+        }
     }
     return cudaErrorNotSupported;
 }

@@ -172,7 +172,7 @@ def test_u32_words_need_small_primes():
         eph.ntt_fwd32(plan, torch.zeros((1, 1, 4096), dtype=torch.int32, device="cuda"))
 
 
-@pytest.mark.parametrize("log2N", [12, 13, 14])
+@pytest.mark.parametrize("log2N", [12, 13, 14, 15, 16])
 @pytest.mark.parametrize("L,batch", [(1, 1), (3, 2), (5, 7), (16, 3), (2, 149), (3, 301), (1, 1000)])
 def test_ntt_c5_u32_kernels(log2N, L, batch):
     """The persistent TMA-fed u32 kernels (ntt32_c5.cu: swizzled in-place passes, TMEM row
