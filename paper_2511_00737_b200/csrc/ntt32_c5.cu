@@ -569,9 +569,10 @@ __global__ void __launch_bounds__(nthreads<LG>(), ctas_per_sm<LG>())
         if constexpr (PF) {   // the next row's H bytes of this thread's slots toward L2 / L1
             const u32 rn = row + gridDim.x;
             if (rn < rows) {
-                const u32 bbn = rn / a.D, dn = rn - bbn * a.D;
+                const u32 bbn = rn / a.D, dn = rn - bbn * a.D, bn = a.b0 + bbn;
                 const u32 q0 = a.k == 1u ? 32u * tid : __umulhi(32u * tid, a.kmagic);
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(H + (size_t)dn * a.nq + (size_t)(a.b0 + bbn) * a.B + q0));
+                if (q0 < min(a.B, a.nq - bn * a.B))   // only bytes the row reads (never past H)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(H + (size_t)dn * a.nq + (size_t)bn * a.B + q0));
             }
         }
         pass_b<LG, true>(B, tws, pr, tid);
