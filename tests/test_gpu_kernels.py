@@ -134,6 +134,34 @@ def test_ntt_c5_two_groups_equal_one_team(log2N, batch):
     assert np.array_equal(_host(d2), x)
 
 
+def test_ntt_c5_cluster_inverse_stress():
+    """The FP64 cluster kernels (DSMEM exchanges, cluster barriers / remote mbarrier
+    signals, the TMA ring) under repetition: 60 forward + inverse launches at seeded
+    random sizes (N = 2^14..2^16, 1..9 primes, 1..300 polynomials), each round trip
+    exact, every fifth through the other warp layout (EPHDC_NTT_ALT_TEAMS: the one-team
+    cluster forward) as well."""
+    rng = np.random.default_rng(4711)
+    plans = {}
+    for it in range(60):
+        log2N = int(rng.integers(14, 17))
+        L = int(rng.integers(1, 10))
+        batch = int(rng.integers(1, 301 if log2N == 14 else 81))
+        key = (log2N, L)
+        if key not in plans:
+            q = nt.prime_chain([48 if log2N == 14 else 44] * L, log2N)
+            plans[key] = (q, eph.NttPlan(q, log2N), eph.NttPlan(q, log2N, alt_teams=True))
+        q, pd, pa = plans[key]
+        x = _dev(inp.gen_residues(q, batch, 1 << log2N, seed=it))
+        d = x.clone()
+        eph.ntt_fwd(pd, d)
+        if it % 5 == 0:
+            g = d.clone()
+            eph.ntt_inv(pa, g)
+            assert torch.equal(g, x), (it, log2N, L, batch)
+        eph.ntt_inv(pd, d)
+        assert torch.equal(d, x), (it, log2N, L, batch)
+
+
 @pytest.mark.parametrize("log2N", [10, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("L", [1, 5, 16])
 def test_ntt_u32_words(log2N, L):
