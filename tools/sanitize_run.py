@@ -1,12 +1,13 @@
 #!/usr/bin/env python
 """One small end-to-end run of the hot path, checked against the oracle's decryption:
 c1q3 by default (N = 1024), every kernel of a call -- encoder, pack+INTT_t, fused
-lift+NTT+MAC, finalize -- plus the noise probe.  EPHDC_F64_FLAGS selects the fused
-kernel's synchronisation variant (4 = the windowed WL = 2 tail that c3/c4 use), so the
-variant runs at a small size.  (Meant for compute-sanitizer; the tool is closed on
-this GPU pool, so it serves as the small-case check with the CPU reference.)
+lift+NTT+MAC, finalize -- plus the noise probe.  --flags sets the ephdc_plan flag bits
+of the fused kernel (4 = the windowed WL = 2 tail that c3/c4 use), so that variant runs
+at a small size.  (Meant for compute-sanitizer; the tool is closed on this GPU pool, so
+it serves as the small-case check against the oracle.  The library reads no
+environment variables: variants go through the plan argument only.)
 
-usage: [EPHDC_F64_FLAGS=4] python tools/sanitize_run.py [--config c1q3] [--nq 700]
+usage: python tools/sanitize_run.py [--config c1q3] [--nq 700] [--flags 4]
 """
 import argparse
 import os
@@ -22,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c1q3")
     ap.add_argument("--nq", type=int, default=700)
+    ap.add_argument("--flags", type=lambda v: int(v, 0), default=0, help="ephdc_plan flag bits (tests / A/B only)")
     a = ap.parse_args()
     import torch
     import ephdc_inputs as inp
@@ -35,7 +37,7 @@ def main():
     ps = ppipe.build(cfg, P, Xtr, ytr)
     X = torch.from_numpy(np.ascontiguousarray(Xq).view(np.int8)).cuda()
     H = eph.encode_queries(ps.ctx, X, ps.P_dev)
-    ws = eph.Workspace(ps.ctx, a.nq)
+    ws = eph.Workspace(ps.ctx, a.nq, plan={"flags": a.flags} if a.flags else None)
     cts = eph.infer_batch(ps.ctx, ps.model, ws, H, a.nq)
     bits, flags, _ = eph.noise_probe(ps.ctx, ps.sk, cts)
     torch.cuda.synchronize()
@@ -43,7 +45,7 @@ def main():
     om = opipe.build_model(cfg, P, Xtr, ytr)
     Sref = hdc.scores(opipe.encode_queries(om, P, Xq), om.class_hv)
     ok = np.array_equal(S, Sref) and not flags.any()
-    print(f"sanitize_run {a.config} nq={a.nq} flags={os.environ.get('EPHDC_F64_FLAGS', '')} "
+    print(f"sanitize_run {a.config} nq={a.nq} plan_flags={a.flags} "
           f"scores {'ok' if ok else 'MISMATCH'} noise_bits={bits.tolist()}")
     return 0 if ok else 1
 
