@@ -789,8 +789,11 @@ EPHDC_D u64 fold128(const U128 &x, u64 q, u64 qinv, u64 r2, u64 r1) {
     const u64 t = mont_mul(x.hi, r2, q, qinv) + mont_mul(x.lo, r1, q, qinv);   // < 2q
     return t >= q ? t - q : t;
 }
+// The D range is cut into dsplit pieces (blockIdx.y); piece y folds into row y / per_slot
+// of out ([slots][L][2][N]; one row, the caller's output, when dsplit <= per_slot), so
+// that a row sums at most per_slot residues < q and cannot wrap 2^64.
 __global__ void __launch_bounds__(256) k_mac(const u64 *__restrict__ ct, const u64 *__restrict__ pt, u32 D, u32 L,
-                                             u32 N, u32 dsplit, PrimeSet ps, u64 *__restrict__ out) {
+                                             u32 N, u32 dsplit, u32 per_slot, PrimeSet ps, u64 *__restrict__ out) {
     const u32 pairs = (L * N) >> 1;
     const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= pairs) return;
@@ -819,7 +822,8 @@ __global__ void __launch_bounds__(256) k_mac(const u64 *__restrict__ ct, const u
         a10 = U128{fold128(a10, q, qinv, r2, r1), 0};
         a11 = U128{fold128(a11, q, qinv, r2, r1), 0};
     }
-    unsigned long long *o = reinterpret_cast<unsigned long long *>(out + (size_t)j * 2 * N + i);
+    unsigned long long *o = reinterpret_cast<unsigned long long *>(
+        out + (size_t)(blockIdx.y / per_slot) * 2 * L * N + (size_t)j * 2 * N + i);
     atomicAdd(o, a00.lo);
     atomicAdd(o + 1, a01.lo);
     atomicAdd(o + N, a10.lo);
@@ -874,6 +878,20 @@ __global__ void k_mod_q(u64 *__restrict__ out, u32 L, u32 N, PrimeSet ps, u32 n_
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_total) return;
     out[i] %= ps.q[(i / N) % L];
+}
+
+// out[i] <- sum over the slot rows of (acc[s][i] mod q_j) mod q_j  (k_mac with slots > 1)
+__global__ void k_mod_q_slots(const u64 *__restrict__ acc, u32 slots, u64 *__restrict__ out, u32 L, u32 N,
+                              PrimeSet ps, u32 n_total) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_total) return;
+    const u64 q = ps.q[(i / N) % L];
+    u64 sum = 0;
+    for (u32 k = 0; k < slots; ++k) {
+        sum += acc[(size_t)k * n_total + i] % q;   // < 2q < 2^62
+        if (sum >= q) sum -= q;
+    }
+    out[i] = sum;
 }
 
 // =====================================================================================
@@ -1282,7 +1300,30 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
         k_mod_q<<<(n + 255) / 256, 256, 0, st>>>(d_out, L, 2 * N, p->ps, n);
         return counted(cudaGetLastError());
     }
-    k_mac<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, d_out);
+    // Integer form (primes >= 2^50): a 64-bit row holds at most max_split = floor(2^64 / q)
+    // partial sums (15 at 60 bits).  When L N is small that many pieces cannot fill the
+    // GPU (L = 1, N = 2^12: 8 x 15 CTAs, 0.48 of HBM, profiles/r02/r67), so the pieces
+    // beyond max_split fold into further rows of a scratch [slots][L][2][N] (<= 1.3 MB:
+    // it is only needed when bx is small) and k_mod_q_slots sums the rows mod q.
+    const u32 want = std::max<u32>(1, std::min(std::min<u32>((148u * 8u + bx - 1) / bx, D), 1u << 16));
+    if (want > max_split) {
+        const u32 slots = (want + max_split - 1) / max_split;
+        u64 *acc = nullptr;
+        e = cudaMallocAsync(reinterpret_cast<void **>(&acc), sizeof(u64) * n * slots, st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(acc, 0, sizeof(u64) * n * slots, st);
+        if (e == cudaSuccess) {
+            k_mac<<<dim3(bx, want), 256, 0, st>>>(d_ct, d_pt, D, L, N, want, max_split, p->ps, acc);
+            e = counted(cudaGetLastError());
+        }
+        if (e == cudaSuccess) {
+            k_mod_q_slots<<<(n + 255) / 256, 256, 0, st>>>(acc, slots, d_out, L, 2 * N, p->ps, n);
+            e = counted(cudaGetLastError());
+        }
+        const cudaError_t e2 = cudaFreeAsync(acc, st);
+        return e != cudaSuccess ? e : e2;
+    }
+    k_mac<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, max_split, p->ps, d_out);
     e = counted(cudaGetLastError());
     if (e != cudaSuccess) return e;
     // output layout [L][2][N]: prime index = i / (2N); the folded sums are true residues

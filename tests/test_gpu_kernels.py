@@ -45,7 +45,9 @@ def test_ntt_fwd_inv_bitexact(log2N, L, bits, force_int):
 
 
 @pytest.mark.parametrize("log2N,L,bits,D", [(12, 3, 60, 5), (13, 5, 44, 64), (14, 9, 48, 33), (12, 16, 60, 300), (12, 2, 61, 130),
-                                            (15, 3, 60, 7), (16, 1, 30, 9), (16, 16, 60, 2)])
+                                            (15, 3, 60, 7), (16, 1, 30, 9), (16, 16, 60, 2),
+                                            # integer form, D split beyond floor(2^64 / q) pieces: slot rows
+                                            (12, 1, 60, 700), (13, 1, 61, 333), (12, 1, 60, 16)])
 def test_mac_bitexact(log2N, L, bits, D):
     N = 1 << log2N
     q = nt.prime_chain([bits] * L, log2N)
