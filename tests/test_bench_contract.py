@@ -56,3 +56,20 @@ def test_product_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_committed_c5_sweep_is_clocked_and_complete():
+    """The committed c5 evidence (profiles/r02/r67/c5_all.jsonl, BASELINE.json configs[4]):
+    every ephdc_inputs.c5_points point is present for NTT and MAC, every line carries a
+    clock record with samples, and no line saw a thermal / hardware slowdown."""
+    import ephdc_inputs as inp
+    path = os.path.join(ROOT, "profiles", "r02", "r67", "c5_all.jsonl")
+    rows = [json.loads(l) for l in open(path) if l.strip().startswith("{")]
+    ntt = {(r["log2N"], r["L"], r["bits"], r["word_bits"] // 8) for r in rows if "ntt_fwd" in r}
+    mac = {(r["log2N"], r["L"], r["bits"], r["word_bits"] // 8) for r in rows if r.get("op") == "mac"}
+    want = {tuple(p[:4]) for p in inp.c5_points("all")}
+    assert ntt == want and mac == want
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    for r in rows:
+        c = r["clocks"]
+        assert c["samples"] >= 1 and c["sm_mhz"] and not (bad & set(c["reasons"])), r
