@@ -1252,6 +1252,15 @@ cudaError_t launch_ntt_batch32(const ephdc_ntt_plan *p, uint32_t *d_polys, uint3
     return ntt_batch_w<u32>(p, d_polys, batch, inverse, st);
 }
 
+// CTAs of two full waves of a 256-thread MAC kernel: the u32 MAC's D split is rounded DOWN
+// to that count, so no third, nearly empty wave forms (r73: 0.88-0.93 -> 1.00-1.04 of HBM
+// at the points whose split had rounded up to 1216 CTAs on 1184 slots).
+template <class K> static u32 two_waves(K kernel) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0) != cudaSuccess || occ < 1) occ = 4;
+    return 2u * 148u * (u32)occ;
+}
+
 cudaError_t launch_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const uint32_t *d_pt, uint32_t D,
                          uint32_t *d_out, cudaStream_t st) {
     const u32 L = p->L, N = p->N;
@@ -1263,7 +1272,7 @@ cudaError_t launch_mac32(const ephdc_ntt_plan *p, const uint32_t *d_ct, const ui
     const u32 quads = (L * N) / 4;
     const u32 bx = (quads + 255) / 256;
     // <= 2^16 partial sums < q < 2^30 per coefficient: the 64-bit fold cannot wrap
-    u32 dsplit = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
+    u32 dsplit = std::max<u32>(1, two_waves(k_mac32) / bx);
     dsplit = std::max<u32>(1, std::min(std::min(dsplit, D), 1u << 16));
     if (e == cudaSuccess && D > 0) {
         k_mac32<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, acc);
@@ -1289,10 +1298,15 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
     u64 qmax = 0;
     for (u32 j = 0; j < L; ++j) qmax = std::max<u64>(qmax, p->q[j]);
     u32 max_split = (u32)std::min<u64>(~0ull / qmax, 1u << 16);
-    u32 dsplit = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
-    dsplit = std::min(std::min(dsplit, D), max_split);
+    const bool f64 = qmax < (1ull << 50);
+    // ~8 CTAs per SM, rounded up.  Rounding down to two full waves (as launch_mac32 does)
+    // was measured on these two kernels too (r74): +4-5 points on average but 1.00 -> 0.86
+    // (FP64 form) and 0.95 -> 0.75 (integer form) at L N >= 2^19, where one piece is left --
+    // not adopted here.
+    const u32 target = std::max<u32>(1, (148u * 8u + bx - 1) / bx);
+    u32 dsplit = std::min(std::min(target, D), max_split);
     const u32 n = 2 * L * N;
-    if (qmax < (1ull << 50)) {   // FP64 pipe: 0.96-1.03 of measured HBM vs 0.74-0.77 (r26, profiles/r02/ab)
+    if (f64) {   // FP64 pipe: 0.96-1.03 of measured HBM vs 0.74-0.77 (r26, profiles/r02/ab)
         const u32 red_every = (u32)std::max<double>(1.0, std::min<double>(64.0, std::floor(4503599627370496.0 / (double)qmax)));
         k_mac_f64<<<dim3(bx, dsplit), 256, 0, st>>>(d_ct, d_pt, D, L, N, dsplit, p->ps, red_every, d_out);
         e = counted(cudaGetLastError());
@@ -1305,7 +1319,7 @@ cudaError_t launch_mac(const ephdc_ntt_plan *p, const uint64_t *d_ct, const uint
     // GPU (L = 1, N = 2^12: 8 x 15 CTAs, 0.48 of HBM, profiles/r02/r67), so the pieces
     // beyond max_split fold into further rows of a scratch [slots][L][2][N] (<= 1.3 MB:
     // it is only needed when bx is small) and k_mod_q_slots sums the rows mod q.
-    const u32 want = std::max<u32>(1, std::min(std::min<u32>((148u * 8u + bx - 1) / bx, D), 1u << 16));
+    const u32 want = std::max<u32>(1, std::min(std::min<u32>(target, D), 1u << 16));
     if (want > max_split) {
         const u32 slots = (want + max_split - 1) / max_split;
         u64 *acc = nullptr;
